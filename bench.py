@@ -1,0 +1,471 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 recursive TRSM/TRMM path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline workload (BASELINE.json configs[2], "C3"): TRSM Left/Lower/NoTrans/
+NonUnit fp64, n = m = 16384 per GPU, alpha = 1, diagonally dominant random A
+(src/bench.cpp:32-61 conditioning); a TRMM Left/Upper/NoTrans fp64 line on
+the same sizes rides along.  GFLOP/s = n^2 * m / t (src/bench.cpp:215-217).
+
+Multi-GPU (torchrun, one process per GPU, NCCL): A is broadcast from rank 0
+inside every timed step, B is column-sharded (m = 16384 columns per GPU,
+weak scaling) with values keyed by the global column; each GPU solves its
+columns with the single-GPU path.  Time = max over ranks.
+
+value : inputs resident in HBM; per-step CUDA events on the launching stream
+        (B restored from a pristine copy between steps, outside the events).
+e2e   : the same call through the C-ABI with pinned HOST buffers (the library
+        stages H2D, computes, copies B back), wall clock per call.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "TRSM/TRMM GFLOP/s (m*n^2) fp64/fp32 at n=16384, % of B200 peak, 1/2/4/8 GPU"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clock and throttle reasons
+    DURING the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - NVML absent
+            log(f"clock sampling unavailable: {e}")
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                mask = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self._nv:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- utilities
+def env_int(k, d):
+    return int(os.environ.get(k, d))
+
+
+def setup_dist(args):
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def allmax(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, world, rank):
+    """`--impl reference`: the reference's own CPU path (oracle/_ref, compiled
+    from the untouched sources) with Backend::par() on every host core, on a
+    bounded column sample of the same workload."""
+    if rank != 0:
+        return
+    import oracle
+    from oracle import ref
+
+    n = args.n
+    m_s = args.ref_cols
+    cores = os.cpu_count()
+    a, b = make_host_inputs(n, m_s, args.op_headline)
+    spec = oracle.spec(0, 0 if args.op_headline == "trsm" else 1, 0, 0, 1.0)
+    if ref.available():
+        kind = "reference"
+
+        def step():
+            st, _, _, _ = ref.rec(args.op_headline, spec, a, b, args.ref_threshold, width=-1)
+            assert st == 0, ref.last_error()
+    else:  # the C restatement (single thread, naive) on a tiny slice
+        kind = "port"
+        m_s = 8
+        b = b[:, :m_s].copy(order="F")
+        cores = 1
+
+        def step():
+            (oracle.oracle_trsm if args.op_headline == "trsm" else oracle.oracle_trmm)(spec, a, b)
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    value = n * n * m_s / t / 1e9
+    sample = (f"{args.op_headline} left-{'lower' if args.op_headline == 'trsm' else 'upper'}-n-nonunit fp64 "
+              f"n={n}, m={m_s} column slice of the m={args.m} workload (columns independent), "
+              f"threshold {args.ref_threshold}, Backend::par() ({cores} threads), median of {args.steps}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def make_host_inputs(n, m, op):
+    """fp64 column-major host inputs, uniform [-1, 1]; TRSM A lower-dominant
+    (src/bench.cpp:40-51)."""
+    rng = np.random.default_rng(42)
+    a = np.asfortranarray(rng.uniform(-1.0, 1.0, (n, n)))
+    if op == "trsm":
+        d = np.zeros(n)
+        for c0 in range(0, n, 2048):  # sum |A(r, c)| over c < r, blockwise
+            blk = np.abs(a[:, c0:c0 + 2048])
+            for j in range(blk.shape[1]):
+                c = c0 + j
+                d[c + 1:] += blk[c + 1:, j]
+        a[np.arange(n), np.arange(n)] = d + 1.0
+    b = np.asfortranarray(rng.uniform(-1.0, 1.0, (n, m)))
+    return a, b
+
+
+def workload_config(args, world):
+    return {
+        "workload": (f"C3 ({args.op_headline} headline): TRSM Left/Lower/NoTrans/NonUnit + TRMM Left/Upper/NoTrans "
+                     f"fp64, n={args.n}, m={args.m} per GPU (m={args.m * world} total), alpha=1, "
+                     "diagonally dominant random A"),
+        "n": args.n, "m_per_gpu": args.m, "m_total": args.m * world, "threshold": args.threshold,
+        "parallelism": f"rhs-shard x{world}" if world > 1 else "single GPU",
+        "l2": "inputs (A 2 GiB + B 2 GiB per GPU) far larger than the 126 MB L2",
+        "timing": "per-step CUDA events on the launching stream; B restored between steps outside the events",
+    }
+
+
+# ----------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--m", type=int, default=16384, help="right-hand sides per GPU")
+    ap.add_argument("--threshold", type=int, default=256)
+    ap.add_argument("--op-headline", choices=["trsm", "trmm"], default="trsm")
+    ap.add_argument("--ref-cols", type=int, default=256)
+    ap.add_argument("--ref-threshold", type=int, default=256)
+    ap.add_argument("--cpu-cols", type=int, default=1024)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cublas", action="store_true")
+    ap.add_argument("--no-trmm", action="store_true")
+    args = ap.parse_args()
+
+    world, rank, local = setup_dist(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    import paper_2504_13821_b200 as rc
+    from paper_2504_13821_b200 import (ASYNC, Backend, Diag, MatrixBuffer, Side, Threshold, Trans,
+                                       TriangularSpec, Uplo)
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    n, m = args.n, args.m
+    f64 = torch.float64
+
+    # Inputs resident in HBM. A: rank 0 generates, broadcast inside each step.
+    A = MatrixBuffer(n, n, f64, dev)
+    if rank == 0:
+        rc.fill_uniform(A.view(), 0, n, seed=1)
+    B = MatrixBuffer(n, m, f64, dev)
+    B0 = MatrixBuffer(n, m, f64, dev)
+    rc.fill_uniform(B0.view(), col0=rank * m, global_rows=n, seed=2)
+    # TRSM reads the lower triangle (diag made dominant); TRMM the upper one.
+    A_trsm = A
+    if rank == 0:
+        rc.make_dominant(A_trsm.view(), Uplo.Lower)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.broadcast(A.data, src=0)
+    be = Backend.cuda(device=local, stream=stream, flags=ASYNC)
+
+    specs = {
+        "trsm": TriangularSpec(Side.Left, Uplo.Lower, Trans.NoTrans, Diag.NonUnit, 1.0),
+        "trmm": TriangularSpec(Side.Left, Uplo.Upper, Trans.NoTrans, Diag.NonUnit, 1.0),
+    }
+    flops_per_gpu = float(n) * n * m
+
+    def one(op):
+        fn = rc.rec_trsm if op == "trsm" else rc.rec_trmm
+        if world > 1:
+            dist.broadcast(A.data, src=0)
+        fn(specs[op], A.cview(), B.view(), Threshold(args.threshold), be)
+
+    def timed(op):
+        for _ in range(args.warmup):
+            B.data.copy_(B0.data)
+            one(op)
+        rc.sync(stream)
+        barrier(world)
+        launches0 = rc.launch_count()
+        evs = []
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                B.data.copy_(B0.data)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                one(op)
+                e1.record(stream)
+                evs.append((e0, e1))
+            rc.sync(stream)
+            torch.cuda.synchronize()
+        launches = rc.launch_count() - launches0
+        barrier(world)
+        local_ms = sum(a.elapsed_time(b) for a, b in evs)
+        ms = allmax(local_ms, world)
+        value = flops_per_gpu * world * args.steps / (ms * 1e-3) / 1e9
+        return value, ms / args.steps, launches, clk.summary()
+
+    peak64 = rc.probe_peak("f64")
+    value, ms_step, launches, clocks = timed("trsm")
+    log(f"trsm: {value:.1f} GFLOP/s, {ms_step:.2f} ms/step, clocks {clocks}")
+
+    # Residual gate on 8 sampled columns (finite check first).
+    B.data.copy_(B0.data)
+    one("trsm")
+    rc.sync(stream)
+    cols = torch.arange(0, m, max(1, m // 8), device=dev)[:8]
+    X = B.data[cols].t()                          # n x 8
+    Bs = B0.data[cols].t()
+    L = torch.tril(A.data.t())                    # masked lower triangle incl. diag
+    resid = (L @ X - Bs).abs().max().item()
+    anorm = L.abs().sum(1).max().item()
+    xmax = X.abs().max().item()
+    eta = resid / (anorm * max(xmax, Bs.abs().max().item(), 1.0) * n * np.finfo(float).eps)
+    finite = bool(torch.isfinite(X).all().item())
+    del L
+    torch.cuda.empty_cache()
+    log(f"residual eta {eta:.3e} finite {finite}")
+
+    trmm = None
+    if not args.no_trmm:
+        tv, tms, tl, tclk = timed("trmm")
+        trmm = {"value": tv, "unit": "GFLOP/s", "ms_per_step": tms, "pct_of_peak": tv / 1e3 / peak64 * 100,
+                "gpu_launches": tl, "clocks": tclk,
+                "workload": f"TRMM Left/Upper/NoTrans/NonUnit fp64 n={n}, m={m} per GPU"}
+        log(f"trmm: {tv:.1f} GFLOP/s, {tms:.2f} ms/step")
+
+    # Per-kernel-class breakdown with CUDA events around every launch (one
+    # extra untimed call, direct launches): the roofline's achieved figure.
+    B.data.copy_(B0.data)
+    torch.cuda.synchronize()
+    rc.profile_enable(True)
+    one("trsm")
+    rc.sync(stream)
+    rc.profile_enable(False)
+    prof = rc.profile_read()
+    g = prof["gemm"]
+    gemm_tflops = g["flops"] / (g["ms"] * 1e-3) / 1e12 if g["ms"] else 0.0
+    step_ms_prof = sum(v["ms"] for v in prof.values())
+    log(f"profile: {json.dumps(prof)}")
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_gemm_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "tensor", "achieved": gemm_tflops, "peak": peak64, "unit": "TFLOP/s",
+        "frac": gemm_tflops / peak64 if peak64 > 0 else None, "traffic": traffic,
+        "kernel": "dgemm_dmma_kernel (off-diagonal GEMM updates, DMMA.8x8x4)",
+        "peak_source": "live DMMA.8x8x4 issue-rate probe on this GPU (rectri_cu_probe_peak; MEASURED_PEAKS.json "
+                       "has no fp64 figure); cf. profiles/r01_microbench_peaks.jsonl",
+        "per_launch_flops": g["flops"] / max(g["launches"], 1), "launches": g["launches"],
+        "share_of_step": g["ms"] / step_ms_prof if step_ms_prof else None,
+        "breakdown_ms": {k: v["ms"] for k, v in prof.items()},
+    }
+
+    # End to end through the C-ABI with pinned host buffers.
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty((n, n), dtype=f64, pin_memory=True)
+        Ah.copy_(A.data)
+        Bh0 = torch.empty((m, n), dtype=f64, pin_memory=True)
+        Bh0.copy_(B0.data)
+        Bh = torch.empty((m, n), dtype=f64, pin_memory=True)
+        Av = rc.MatrixView(Ah, n, n).as_const()
+        Bv = rc.MatrixView(Bh, n, m)
+        be_sync = Backend.cuda(device=local, stream=stream)
+        walls = []
+        for i in range(args.warmup + args.steps):
+            Bh.copy_(Bh0)
+            barrier(world)
+            t0 = time.perf_counter()
+            rc.rec_trsm(specs["trsm"], Av, Bv, Threshold(args.threshold), be_sync)
+            w = time.perf_counter() - t0
+            if i >= args.warmup:
+                walls.append(w)
+        wall = allmax(sum(walls), world)
+        e2e = {"value": flops_per_gpu * world * args.steps / wall / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": (n * n + n * m) * 8 * world, "d2h_bytes_per_step": n * m * 8 * world,
+               "ms_per_step": wall / args.steps * 1e3,
+               "path": "rectri_cu_rec_trsm_f64 with pinned host views (H2D A+B, compute, D2H B), wall clock"}
+        log(f"e2e: {e2e['value']:.1f} GFLOP/s")
+        del Ah, Bh, Bh0
+
+    # cuBLAS reported comparison (same inputs, device-resident).
+    cublas = None
+    if not args.no_cublas and world == 1:
+        try:
+            cublas = cublas_compare(A, B0, n, m, args)
+        except Exception as e:  # pragma: no cover
+            cublas = {"error": str(e)}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1 and rank == 0:
+        cpu = cpu_baseline(args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated uniform[-1,1), dominant A)",
+            "config": workload_config(args, world),
+            "pct_of_peak": value / 1e3 / (peak64 * world) * 100,
+            "residual": {"eta": eta, "finite": finite, "bound": 32,
+                         "definition": "||tril(A) X - B||_max / (||A||_inf max(|X|,|B|,1) n eps), 8 sampled columns"},
+            "trmm": trmm, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "cublas": cublas,
+            "clocks": clocks, "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cublas_compare(A, B0, n, m, args):
+    """cuBLAS dtrsm (torch.linalg.solve_triangular) and dgemm (torch.mm) on
+    the same device inputs, as a reported comparison only."""
+    out = {}
+    Am = A.data.t()  # (n, n) logical matrix view
+    L = torch.tril(Am)
+    Bm = B0.data.t()
+    torch.cuda.synchronize()
+    for name, fn in (("dtrsm_LLN", lambda: torch.linalg.solve_triangular(L, Bm, upper=False)),
+                     ("dgemm", lambda: torch.mm(L, Bm))):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        fl = float(n) * n * m * (2 if name == "dgemm" else 1)
+        out[name] = {"ms": ms, "gflops": fl / ms / 1e6, "flops_counted": "2n^2m" if name == "dgemm" else "n^2m"}
+        del r
+    del L
+    torch.cuda.empty_cache()
+    return out
+
+
+def cpu_baseline(args):
+    """The reference's CPU path (oracle/_ref) on the host cores, bounded sample."""
+    import oracle
+    from oracle import ref
+
+    n, m_s = args.n, args.cpu_cols
+    a, b = make_host_inputs(n, m_s, "trsm")
+    spec = oracle.spec(0, 0, 0, 0, 1.0)
+    if ref.available():
+        ref.rec("trsm", spec, a, b[:, :16].copy(order="F"), 256, width=-1)  # warm
+        t0 = time.perf_counter()
+        st, _, _, _ = ref.rec("trsm", spec, a, b, 256, width=-1)
+        t = time.perf_counter() - t0
+        assert st == 0
+        return {"value": n * n * m_s / t / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"rec_trsm left-lower-n-nonunit fp64 n={n}, m={m_s} column slice, threshold 256, "
+                          f"Backend::par() ({os.cpu_count()} threads), one call ({t:.1f} s)"}
+    m_s = 4
+    t0 = time.perf_counter()
+    oracle.oracle_trsm(spec, a, b[:, :m_s].copy(order="F"))
+    t = time.perf_counter() - t0
+    return {"value": n * n * m_s / t / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
+            "sample": f"C oracle restatement, n={n}, m={m_s}"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,60 @@
+// common.cuh -- shared device helpers for the sm_100a TRMM/TRSM kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rectri_cu {
+
+using i64 = int64_t;
+
+// ---------------------------------------------------------------------------
+// cp.async (LDGSTS).  `src_bytes` < cp size zero-fills the remainder, which is
+// how every out-of-range element of a tile becomes an exact 0 (never a
+// multiply-by-mask: NaN must not leak from outside a view).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---------------------------------------------------------------------------
+// fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col), lowered to SASS
+// DMMA.8x8x4 on sm_100a (tcgen05 has no f64 kind).  Fragment ownership
+// (lane = 4*g + t): a = A[g][t], b = B[t][g], c{0,1} = C[g][2t + {0,1}].
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
+// Swizzled shared-memory tile addressing for 8-byte elements.  A tile row of
+// `width` doubles (width % 16 == 0) is split into 16-byte chunks; the chunk
+// index is XORed with 2*(row & 3).  With the m8n8k4 fragment pattern (8
+// consecutive outer indices x 4 consecutive k) every half-warp then touches 16
+// distinct 8-byte banks whether the tile is stored k-major or outer-major, and
+// 16-byte cp.async chunks stay intact.
+__device__ __forceinline__ int swz64(int row, int col, int width) {
+  return row * width + ((((col >> 1) ^ ((row & 3) << 1))) << 1) + (col & 1);
+}
+
+__host__ __device__ __forceinline__ i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
+
+}  // namespace rectri_cu

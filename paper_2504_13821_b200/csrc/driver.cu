@@ -1,0 +1,984 @@
+// driver.cu -- host side of the B200 TRMM/TRSM library and its C-ABI.
+//
+// Mirrors the reference's recursion driver (src/recursion.cpp:48-192) on
+// the host: the same validation order (check_problem, :50-67), the same
+// schema table (schema_for, :18-46), the same split at floor(n/2)
+// (matrix.hpp:180-183) and the same event sequence (:94, :97, :139) -- but
+// instead of computing, each node ENQUEUES one sm_100a kernel (leaf or GEMM)
+// on a CUDA stream.  The launch sequence of a (problem, buffers) key is
+// captured once into a CUDA graph and replayed on later calls, with the
+// recorded event list replayed to the caller's sink.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <list>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <type_traits>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/rectri_cu.h"
+#include "launch.h"
+
+namespace rectri_cu {
+namespace {
+
+// ---------------------------------------------------------------------------
+// Errors: every reference exception type is one status code.
+struct Fail {
+  int code;
+  std::string msg;
+  i64 index = -1;
+};
+
+thread_local std::string g_last_error;
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Fail{code, buf};
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(RECTRI_CU_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+template <typename F>
+int guarded(F&& f, i64* index_out) {
+  try {
+    f();
+    return RECTRI_CU_OK;
+  } catch (const Fail& e) {
+    g_last_error = e.msg;
+    if (e.code == RECTRI_CU_SINGULAR && index_out) *index_out = e.index;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return RECTRI_CU_CUDA;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Boundary types.
+enum OpK { kTrmm = 0, kTrsm = 1 };
+
+const char* side_name(int s) { return s == RECTRI_CU_LEFT ? "left" : "right"; }
+
+struct Spec {
+  int side, uplo, trans, diag;  // trans already reduced: 0 = N, 1 = T
+  double alpha;
+};
+
+Spec validate_spec(const rectri_cu_spec* s) {
+  if (!s) fail(RECTRI_CU_CONFIG, "spec must not be null");
+  if (s->side < 0 || s->side > 1 || s->uplo < 0 || s->uplo > 1 || s->trans < 0 || s->trans > 2 ||
+      s->diag < 0 || s->diag > 1)
+    fail(RECTRI_CU_CONFIG, "spec flag out of range");
+  // flags.hpp:47-49
+  if (!std::isfinite(s->alpha)) fail(RECTRI_CU_CONFIG, "alpha must be finite");
+  // ConjTrans == Trans on real element kinds (flags.hpp:38-45).
+  return Spec{s->side, s->uplo, s->trans == RECTRI_CU_NOTRANS ? 0 : 1, s->diag, s->alpha};
+}
+
+struct BackendInfo {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  unsigned flags = 0;
+};
+
+BackendInfo validate_backend(const rectri_cu_backend* b) {
+  BackendInfo out;
+  if (!b) return out;  // Backend{} defaults
+  // backend.hpp:31-37
+  if (b->parallel_width < 1) fail(RECTRI_CU_CONFIG, "backend parallel_width must be >= 1");
+  if (b->mc < 1 || b->kc < 1 || b->nc < 1)
+    fail(RECTRI_CU_CONFIG, "backend block sizes must be >= 1");
+  out.device = b->device;
+  out.stream = static_cast<cudaStream_t>(b->stream);
+  out.flags = b->flags;
+  return out;
+}
+
+void validate_view(const rectri_cu_view& v, const char* name) {
+  if (v.rows < 0 || v.cols < 0 || v.row_offset < 0 || v.col_offset < 0 ||
+      v.row_offset + v.rows > v.origin_rows || v.col_offset + v.cols > v.origin_cols)
+    fail(RECTRI_CU_BOUNDS, "view %s escapes its origin", name);
+}
+
+bool view_empty(const rectri_cu_view& v) { return v.rows == 0 || v.cols == 0; }
+
+// matrix.hpp:168-177
+bool overlaps(const rectri_cu_view& a, const rectri_cu_view& b) {
+  if (a.origin != b.origin) return false;
+  if (view_empty(a) || view_empty(b)) return false;
+  const bool rows_meet = a.row_offset < b.row_offset + b.rows && b.row_offset < a.row_offset + a.rows;
+  const bool cols_meet = a.col_offset < b.col_offset + b.cols && b.col_offset < a.col_offset + a.cols;
+  return rows_meet && cols_meet;
+}
+
+template <typename T>
+struct DView {
+  T* p;
+  i64 ld, rows, cols;
+  DView sub(i64 r0, i64 c0, i64 nr, i64 nc) const { return DView{p + c0 * ld + r0, ld, nr, nc}; }
+  operator DView<const T>() const { return DView<const T>{p, ld, rows, cols}; }
+};
+
+template <typename T>
+DView<T> dview_of(const rectri_cu_view& v) {
+  T* base = static_cast<T*>(v.origin);
+  return DView<T>{base + v.col_offset * v.origin_rows + v.row_offset, v.origin_rows, v.rows, v.cols};
+}
+
+bool is_device_memory(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ---------------------------------------------------------------------------
+// Recursion schema (recursion.cpp:18-46), verbatim rule.
+struct Schema {
+  bool first_a22;
+  int off_trans;
+  bool off_on_left;
+  bool read_b2, write_b2;
+  double sign;
+  bool carries_alpha;
+};
+
+Schema schema_for(OpK op, int side, int uplo, int trans) {
+  const bool straight = (uplo == RECTRI_CU_LOWER) == (trans == 0);
+  const bool flip_for_op = op == kTrsm;
+  const bool flip_for_side = side == RECTRI_CU_RIGHT;
+  const bool first_is_a22 = (straight != flip_for_op) != flip_for_side;
+  Schema s;
+  s.first_a22 = first_is_a22;
+  s.off_trans = trans;
+  s.off_on_left = side == RECTRI_CU_LEFT;
+  const bool first_b2 = first_is_a22;
+  if (op == kTrmm) {
+    s.write_b2 = first_b2;
+    s.read_b2 = !first_b2;
+    s.sign = 1.0;
+    s.carries_alpha = true;
+  } else {
+    s.read_b2 = first_b2;
+    s.write_b2 = !first_b2;
+    s.sign = -1.0;
+    s.carries_alpha = false;
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// Kernel launch shims per element type.
+template <typename T>
+struct K;
+template <>
+struct K<double> {
+  static void gemm(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s) {
+    launch_gemm_f64(p, ta, tb, s);
+  }
+  static void leaf(const LeafParams<double>& p, cudaStream_t s) { launch_leaf_f64(p, s); }
+  static void scale(double* B, i64 ld, i64 r, i64 c, double a, cudaStream_t s) {
+    launch_scale_f64(B, ld, r, c, a, s);
+  }
+  static void scan(const double* A, i64 lda, i64 n, uint8_t* f, cudaStream_t s) {
+    launch_diag_zero_scan_f64(A, lda, n, f, s);
+  }
+};
+template <>
+struct K<float> {
+  static void gemm(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
+    launch_gemm_f32(p, ta, tb, s);
+  }
+  static void leaf(const LeafParams<float>& p, cudaStream_t s) { launch_leaf_f32(p, s); }
+  static void scale(float* B, i64 ld, i64 r, i64 c, float a, cudaStream_t s) {
+    launch_scale_f32(B, ld, r, c, a, s);
+  }
+  static void scan(const float* A, i64 lda, i64 n, uint8_t* f, cudaStream_t s) {
+    launch_diag_zero_scan_f32(A, lda, n, f, s);
+  }
+};
+
+struct Ev {
+  int32_t e;
+  i64 n, m;
+};
+
+// Per-kernel-class event profiling (rectri_cu_profile_*).
+struct ProfRec {
+  int kind;
+  double flops;
+  cudaEvent_t a, b;
+};
+struct Profiler {
+  bool on = false;
+  std::vector<ProfRec> recs;
+};
+Profiler g_prof;
+
+struct ProfScope {
+  ProfRec rec{};
+  cudaStream_t s;
+  bool active;
+  ProfScope(int kind, double flops, cudaStream_t s_) : s(s_), active(g_prof.on) {
+    if (!active) return;
+    rec.kind = kind;
+    rec.flops = flops;
+    cudaEventCreate(&rec.a);
+    cudaEventCreate(&rec.b);
+    cudaEventRecord(rec.a, s);
+  }
+  ~ProfScope() {
+    if (!active) return;
+    cudaEventRecord(rec.b, s);
+    g_prof.recs.push_back(rec);
+  }
+};
+
+// Enqueues C <- alpha * op(A) * op(B) + beta * C (gemm.cpp:155-216 minus
+// validation): alpha == 0 or K == 0 only applies beta.
+template <typename T>
+void enqueue_gemm(T alpha, bool ta, DView<const T> A, bool tb, DView<const T> B, T beta,
+                  DView<T> C, cudaStream_t s) {
+  const i64 M = C.rows, N = C.cols, Kd = ta ? A.rows : A.cols;
+  if (M == 0 || N == 0) return;
+  if (alpha == T(0) || Kd == 0) {  // apply_beta (gemm.cpp:129-142)
+    if (beta == T(0))
+      cuda_check(cudaMemset2DAsync(C.p, sizeof(T) * C.ld, 0, sizeof(T) * M, N, s), "zero C");
+    else if (beta != T(1))
+      K<T>::scale(C.p, C.ld, M, N, beta, s);
+    return;
+  }
+  GemmParams<T> p{M, N, Kd, alpha, beta, A.p, A.ld, B.p, B.ld, C.p, C.ld};
+  ProfScope prof(0, 2.0 * static_cast<double>(M) * N * Kd, s);
+  K<T>::gemm(p, ta, tb, s);
+}
+
+// One base-kernel call on the device (base_kernels.cpp:137-177 minus
+// validation and the zero-pivot scan).  Tiles above kLeafMax are solved by an
+// internal recursion with the same schema (no events: semantically one call).
+template <typename T>
+void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s);
+
+template <typename T>
+class Recursion {
+ public:
+  Recursion(OpK op, i64 threshold, cudaStream_t s, std::vector<Ev>* events,
+            std::vector<std::pair<i64, i64>>* leaves)
+      : op_(op), threshold_(threshold), s_(s), events_(events), leaves_(leaves) {}
+
+  // recursion.cpp:85-148
+  void run(const Spec& spec, DView<const T> A, DView<T> B, i64 row0) {
+    const i64 n = A.rows;
+    const i64 rhs = spec.side == RECTRI_CU_LEFT ? B.cols : B.rows;
+    if (n <= threshold_) {
+      emit(op_ == kTrmm ? RECTRI_CU_EV_BASE_TRMM : RECTRI_CU_EV_BASE_TRSM, n, rhs);
+      if (leaves_) leaves_->push_back({row0, n});
+      enqueue_base<T>(op_, spec, A, B, s_);
+      return;
+    }
+    const i64 mid = n / 2;  // split_half
+    const Schema sc = schema_for(op_, spec.side, spec.uplo, spec.trans);
+    const DView<const T> a11 = A.sub(0, 0, mid, mid);
+    const DView<const T> a22 = A.sub(mid, mid, n - mid, n - mid);
+    const DView<const T> off =
+        spec.uplo == RECTRI_CU_LOWER ? A.sub(mid, 0, n - mid, mid) : A.sub(0, mid, mid, n - mid);
+    const bool left = spec.side == RECTRI_CU_LEFT;
+    const DView<T> b1 = left ? B.sub(0, 0, mid, B.cols) : B.sub(0, 0, B.rows, mid);
+    const DView<T> b2 = left ? B.sub(mid, 0, n - mid, B.cols) : B.sub(0, mid, B.rows, n - mid);
+
+    if (sc.first_a22) run(spec, a22, b2, row0 + mid);
+    else run(spec, a11, b1, row0);
+
+    const DView<T> dst = sc.write_b2 ? b2 : b1;
+    const DView<const T> src = sc.read_b2 ? b2 : b1;
+    const T coeff = static_cast<T>(sc.sign * (sc.carries_alpha ? spec.alpha : 1.0));
+    emit(RECTRI_CU_EV_GEMM, dst.rows, dst.cols);
+    if (sc.off_on_left)
+      enqueue_gemm<T>(coeff, sc.off_trans != 0, off, false, src, T(1), dst, s_);
+    else
+      enqueue_gemm<T>(coeff, false, src, sc.off_trans != 0, off, T(1), dst, s_);
+
+    if (sc.first_a22) run(spec, a11, b1, row0);
+    else run(spec, a22, b2, row0 + mid);
+  }
+
+ private:
+  void emit(int32_t e, i64 n, i64 m) {
+    if (events_) events_->push_back(Ev{e, n, m});
+  }
+  OpK op_;
+  i64 threshold_;
+  cudaStream_t s_;
+  std::vector<Ev>* events_;
+  std::vector<std::pair<i64, i64>>* leaves_;
+};
+
+template <typename T>
+void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s) {
+  const i64 n = A.rows;
+  const bool left = spec.side == RECTRI_CU_LEFT;
+  const i64 rhs = left ? B.cols : B.rows;
+  if (n == 0 || rhs == 0) return;
+  if (n > kLeafMax) {
+    Recursion<T>(op, kLeafMax, s, nullptr, nullptr).run(spec, A, B, 0);
+    return;
+  }
+  // Right is Left on the transposed problem with op flipped (base_kernels.cpp:152-155).
+  const int eff = left ? spec.trans : 1 - spec.trans;
+  LeafParams<T> p;
+  p.n = static_cast<int>(n);
+  p.nrhs = rhs;
+  p.A = A.p;
+  p.lda = A.ld;
+  p.B = B.p;
+  p.ldb = B.ld;
+  p.right = left ? 0 : 1;
+  p.reflected = (spec.uplo == RECTRI_CU_LOWER) == (eff == 1) ? 1 : 0;
+  p.swapped = eff == 1 ? 1 : 0;
+  p.unit = spec.diag == RECTRI_CU_UNIT ? 1 : 0;
+  p.trsm = op == kTrsm ? 1 : 0;
+  p.alpha = static_cast<T>(spec.alpha);
+  ProfScope prof(1, static_cast<double>(n) * n * rhs, s);
+  K<T>::leaf(p, s);
+}
+
+// ---------------------------------------------------------------------------
+// Per-device resources: capture stream and a staging pool for host views.
+struct DeviceRes {
+  cudaStream_t capture = nullptr;
+  void* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes[2] = {0, 0};
+};
+
+std::mutex g_mu;
+std::map<int, DeviceRes> g_dev;
+
+DeviceRes& device_res(int dev) {
+  DeviceRes& r = g_dev[dev];
+  if (!r.capture) cuda_check(cudaStreamCreateWithFlags(&r.capture, cudaStreamNonBlocking), "stream");
+  return r;
+}
+
+void* staging(DeviceRes& r, int slot, size_t bytes) {
+  if (r.stage_bytes[slot] < bytes) {
+    if (r.stage[slot]) cudaFree(r.stage[slot]);
+    r.stage[slot] = nullptr;
+    r.stage_bytes[slot] = 0;
+    cuda_check(cudaMalloc(&r.stage[slot], bytes), "staging alloc");
+    r.stage_bytes[slot] = bytes;
+  }
+  return r.stage[slot];
+}
+
+// ---------------------------------------------------------------------------
+// Graph cache.
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<Ev> events;
+  std::vector<std::pair<i64, i64>> leaves;
+  uint8_t* d_flags = nullptr;
+  uint8_t* h_flags = nullptr;
+  i64 nodes = 0;
+  int device = 0;
+  ~GraphEntry() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (d_flags) cudaFree(d_flags);
+    if (h_flags) cudaFreeHost(h_flags);
+  }
+};
+
+using Key = std::tuple<int, int, int, int, int, int, uint64_t, const void*, i64, i64, void*, i64,
+                       i64, i64, i64, int>;
+
+struct Cache {
+  std::list<std::pair<Key, std::shared_ptr<GraphEntry>>> lru;
+  std::map<Key, decltype(lru)::iterator> index;
+  static constexpr size_t kCap = 64;
+  std::shared_ptr<GraphEntry> get(const Key& k) {
+    auto it = index.find(k);
+    if (it == index.end()) return nullptr;
+    lru.splice(lru.begin(), lru, it->second);
+    return it->second->second;
+  }
+  void put(const Key& k, std::shared_ptr<GraphEntry> e) {
+    lru.emplace_front(k, std::move(e));
+    index[k] = lru.begin();
+    while (lru.size() > kCap) {
+      index.erase(lru.back().first);
+      lru.pop_back();
+    }
+  }
+  void clear() {
+    index.clear();
+    lru.clear();
+  }
+};
+Cache g_cache;
+
+// Pending singularity checks for RECTRI_CU_ASYNC calls, per stream.
+std::multimap<cudaStream_t, std::shared_ptr<GraphEntry>> g_pending;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+i64 first_singular(const GraphEntry& g) {
+  for (const auto& leaf : g.leaves)
+    for (i64 r = leaf.first; r < leaf.first + leaf.second; ++r)
+      if (g.h_flags[r]) return r;
+  return -1;
+}
+
+// Builds (captures) the whole device-side call: alpha pre-scale (TRSM,
+// recursion.cpp:185-189), the zero-pivot pre-scan (TRSM NonUnit), and the
+// recursion.  Runs on `s` directly when `capture` is false.
+template <typename T>
+std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DView<T> B,
+                                  i64 threshold, cudaStream_t s, bool capture, int dev) {
+  auto g = std::make_shared<GraphEntry>();
+  g->device = dev;
+  const bool scan = op == kTrsm && spec.diag == RECTRI_CU_NONUNIT;
+  if (scan) {
+    cuda_check(cudaMalloc(&g->d_flags, static_cast<size_t>(A.rows)), "flags alloc");
+    cuda_check(cudaMallocHost(&g->h_flags, static_cast<size_t>(A.rows)), "flags alloc");
+  }
+  Spec eff = spec;
+  i64& counter = launch_counter();
+  const i64 before = counter;
+  if (capture) cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+  if (op == kTrsm) {
+    if (spec.alpha != 1.0) {
+      ProfScope prof(2, 0.0, s);
+      K<T>::scale(B.p, B.ld, B.rows, B.cols, static_cast<T>(spec.alpha), s);
+    }
+    eff.alpha = 1.0;
+  }
+  if (scan) {
+    ProfScope prof(3, 0.0, s);
+    K<T>::scan(A.p, A.ld, A.rows, g->d_flags, s);
+    cudaMemcpyAsync(g->h_flags, g->d_flags, static_cast<size_t>(A.rows), cudaMemcpyDeviceToHost, s);
+  }
+  Recursion<T>(op, threshold, s, &g->events, &g->leaves).run(eff, A, B, 0);
+  cudaError_t le = cudaGetLastError();
+  if (capture) {
+    cudaGraph_t graph = nullptr;
+    cudaError_t ee = cudaStreamEndCapture(s, &graph);
+    if (le != cudaSuccess) cuda_check(le, "launch during capture");
+    cuda_check(ee, "end capture");
+    cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    cuda_check(ie, "graph instantiate");
+    g->nodes = counter - before;
+    counter = before;  // counted when replayed
+  } else {
+    cuda_check(le, "kernel launch");
+  }
+  return g;
+}
+
+template <typename T>
+int dtype_code();
+template <>
+int dtype_code<double>() { return 1; }
+template <>
+int dtype_code<float>() { return 0; }
+
+uint64_t bits_of(double a) {
+  uint64_t b;
+  std::memcpy(&b, &a, sizeof b);
+  return b;
+}
+
+// Device-resident recursive call (both views on the device of `dev`).
+template <typename T>
+void run_device(OpK op, const Spec& spec, DView<const T> A, DView<T> B, i64 threshold,
+                const BackendInfo& be, rectri_cu_event_fn sink, void* user, int dev,
+                bool force_sync) {
+  cudaStream_t user_s = be.stream;
+  const bool async = (be.flags & RECTRI_CU_ASYNC) && !force_sync;
+  std::shared_ptr<GraphEntry> g;
+  if ((be.flags & RECTRI_CU_NO_GRAPH) || g_prof.on) {
+    g = build<T>(op, spec, A, B, threshold, user_s, false, dev);
+    for (const Ev& e : g->events)
+      if (sink) sink(user, e.e, e.n, e.m);
+  } else {
+    const Key key{static_cast<int>(op), dtype_code<T>(), spec.side, spec.uplo, spec.trans,
+                  spec.diag, bits_of(spec.alpha), static_cast<const void*>(A.p), A.ld, A.rows,
+                  static_cast<void*>(B.p), B.ld, B.rows, B.cols, threshold, dev};
+    {
+      std::lock_guard<std::mutex> lock(g_mu);
+      g = g_cache.get(key);
+      if (!g) {
+        DeviceRes& res = device_res(dev);
+        g = build<T>(op, spec, A, B, threshold, res.capture, true, dev);
+        g_cache.put(key, g);
+      }
+    }
+    for (const Ev& e : g->events)
+      if (sink) sink(user, e.e, e.n, e.m);
+    cuda_check(cudaGraphLaunch(g->exec, user_s), "graph launch");
+    launch_counter() += g->nodes;
+  }
+  if (async) {
+    if (g->h_flags) {
+      std::lock_guard<std::mutex> lock(g_mu);
+      g_pending.emplace(user_s, g);
+    }
+    return;
+  }
+  cuda_check(cudaStreamSynchronize(user_s), "synchronize");
+  if (g->h_flags) {
+    const i64 r = first_singular(*g);
+    if (r >= 0) {
+      Fail f{RECTRI_CU_SINGULAR, "singular triangular matrix: zero diagonal at row " + std::to_string(r)};
+      f.index = r;
+      throw f;
+    }
+  }
+}
+
+// rec_trmm / rec_trsm entry (recursion.cpp:165-192).
+template <typename T>
+void rec_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
+               const rectri_cu_view& Bv, i64 threshold, const rectri_cu_backend* cbe,
+               rectri_cu_event_fn sink, void* user) {
+  validate_view(Av, "A");
+  validate_view(Bv, "B");
+  // check_problem (recursion.cpp:50-67): spec, backend, threshold, square,
+  // conformal, alias -- in that order.
+  const Spec spec = validate_spec(cspec);
+  const BackendInfo be = validate_backend(cbe);
+  if (threshold < 1) fail(RECTRI_CU_CONFIG, "threshold must be >= 1");
+  if (Av.rows != Av.cols)
+    fail(RECTRI_CU_SHAPE, "triangular A must be square, got %lldx%lld", (long long)Av.rows,
+         (long long)Av.cols);
+  const i64 want = spec.side == RECTRI_CU_LEFT ? Bv.rows : Bv.cols;
+  if (want != Av.rows)
+    fail(RECTRI_CU_SHAPE, "B is %lldx%lld, not conformal with %lldx%lld A on the %s",
+         (long long)Bv.rows, (long long)Bv.cols, (long long)Av.rows, (long long)Av.cols,
+         side_name(spec.side));
+  if (overlaps(Av, Bv)) fail(RECTRI_CU_ALIAS, "A and B views overlap");
+  if (Av.rows == 0 || Bv.rows == 0 || Bv.cols == 0) return;
+
+  DeviceGuard guard(be.device);
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  const bool a_dev = is_device_memory(Av.origin);
+  const bool b_dev = is_device_memory(Bv.origin);
+  if (a_dev && b_dev) {
+    run_device<T>(op, spec, dview_of<const T>(Av), dview_of<T>(Bv), threshold, be, sink, user,
+                  dev, false);
+    return;
+  }
+  // Host-resident operands: stage to the device, compute, copy B back.
+  const i64 n = Av.rows;
+  cudaStream_t s = be.stream;
+  DView<const T> A = dview_of<const T>(Av);
+  DView<T> B = dview_of<T>(Bv);
+  DView<const T> dA = A;
+  DView<T> dB = B;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    DeviceRes& res = device_res(dev);
+    if (!a_dev) {
+      T* p = static_cast<T*>(staging(res, 0, static_cast<size_t>(n * n) * sizeof(T)));
+      dA = DView<const T>{p, n, n, n};
+    }
+    if (!b_dev) {
+      T* p = static_cast<T*>(staging(res, 1, static_cast<size_t>(B.rows * B.cols) * sizeof(T)));
+      dB = DView<T>{p, B.rows, B.rows, B.cols};
+    }
+  }
+  if (!a_dev)
+    cuda_check(cudaMemcpy2DAsync(const_cast<T*>(dA.p), sizeof(T) * n, A.p, sizeof(T) * A.ld,
+                                 sizeof(T) * n, n, cudaMemcpyHostToDevice, s),
+               "H2D A");
+  if (!b_dev)
+    cuda_check(cudaMemcpy2DAsync(dB.p, sizeof(T) * dB.ld, B.p, sizeof(T) * B.ld,
+                                 sizeof(T) * B.rows, B.cols, cudaMemcpyHostToDevice, s),
+               "H2D B");
+  BackendInfo be2 = be;
+  be2.flags &= ~RECTRI_CU_ASYNC;
+  try {
+    run_device<T>(op, spec, dA, dB, threshold, be2, sink, user, dev, true);
+  } catch (const Fail& f) {
+    if (f.code != RECTRI_CU_SINGULAR) throw;
+    // B is unspecified after a singularity error; leave the host copy as is.
+    throw;
+  }
+  if (!b_dev) {
+    cuda_check(cudaMemcpy2DAsync(B.p, sizeof(T) * B.ld, dB.p, sizeof(T) * dB.ld,
+                                 sizeof(T) * B.rows, B.cols, cudaMemcpyDeviceToHost, s),
+               "D2H B");
+    cuda_check(cudaStreamSynchronize(s), "synchronize");
+  }
+}
+
+// Temporary device copies of host views for the non-recursive entry points.
+template <typename T>
+struct Staged {
+  using U = std::remove_const_t<T>;
+  DView<T> view{};
+  U* dev = nullptr;
+  const T* host = nullptr;
+  i64 host_ld = 0;
+  Staged(const rectri_cu_view& v, cudaStream_t s) {
+    DView<T> h = dview_of<T>(v);
+    if (view_empty(v) || is_device_memory(v.origin)) {
+      view = h;
+      return;
+    }
+    host = h.p;
+    host_ld = h.ld;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&dev), static_cast<size_t>(h.rows * h.cols) * sizeof(T) + 16), "stage");
+    view = DView<T>{dev, h.rows, h.rows, h.cols};
+    cuda_check(cudaMemcpy2DAsync(dev, sizeof(T) * h.rows, h.p, sizeof(T) * h.ld,
+                                 sizeof(T) * h.rows, h.cols, cudaMemcpyHostToDevice, s),
+               "H2D");
+  }
+  void copy_back(cudaStream_t s) {
+    if (!dev) return;
+    cuda_check(cudaMemcpy2DAsync(const_cast<T*>(host), sizeof(T) * host_ld, dev,
+                                 sizeof(T) * view.ld, sizeof(T) * view.rows, view.cols,
+                                 cudaMemcpyDeviceToHost, s),
+               "D2H");
+  }
+  ~Staged() {
+    if (dev) cudaFree(dev);
+  }
+};
+
+// trsm_base / trmm_base entry (base_kernels.cpp:16-33, 137-177).
+template <typename T>
+void base_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
+                const rectri_cu_view& Bv, i64 tile_limit, const rectri_cu_backend* cbe) {
+  validate_view(Av, "A");
+  validate_view(Bv, "B");
+  // check_tile (base_kernels.cpp:16-33), then validate(backend).
+  const Spec spec = validate_spec(cspec);
+  if (Av.rows != Av.cols)
+    fail(RECTRI_CU_SHAPE, "triangular A must be square, got %lldx%lld", (long long)Av.rows,
+         (long long)Av.cols);
+  const i64 want = spec.side == RECTRI_CU_LEFT ? Bv.rows : Bv.cols;
+  if (want != Av.rows)
+    fail(RECTRI_CU_SHAPE, "B is %lldx%lld, not conformal with %lldx%lld A on the %s",
+         (long long)Bv.rows, (long long)Bv.cols, (long long)Av.rows, (long long)Av.cols,
+         side_name(spec.side));
+  if (Av.rows > tile_limit)
+    fail(RECTRI_CU_TILE_LIMIT, "tile of size %lld exceeds limit %lld", (long long)Av.rows,
+         (long long)tile_limit);
+  if (overlaps(Av, Bv)) fail(RECTRI_CU_ALIAS, "A and B views overlap");
+  const BackendInfo be = validate_backend(cbe);
+  const i64 n = Av.rows;
+  const i64 rhs = spec.side == RECTRI_CU_LEFT ? Bv.cols : Bv.rows;
+
+  DeviceGuard guard(be.device);
+  cudaStream_t s = be.stream;
+  if (op == kTrsm && spec.diag == RECTRI_CU_NONUNIT && n > 0) {
+    // Zero pivots are found before B is touched (base_kernels.cpp:166-169).
+    Staged<const T> A(Av, s);
+    uint8_t* d = nullptr;
+    cuda_check(cudaMalloc(&d, static_cast<size_t>(n)), "flags");
+    std::vector<uint8_t> h(static_cast<size_t>(n));
+    K<T>::scan(A.view.p, A.view.ld, n, d, s);
+    cudaError_t e = cudaMemcpyAsync(h.data(), d, static_cast<size_t>(n), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(d);
+    cuda_check(e, "pivot scan");
+    for (i64 r = 0; r < n; ++r)
+      if (h[static_cast<size_t>(r)]) {
+        Fail f{RECTRI_CU_SINGULAR, "singular triangular matrix: zero diagonal at row " + std::to_string(r)};
+        f.index = r;
+        throw f;
+      }
+  }
+  if (n == 0 || rhs == 0) return;
+  Staged<const T> A(Av, s);
+  Staged<T> B(Bv, s);
+  enqueue_base<T>(op, spec, A.view, B.view, s);
+  cuda_check(cudaGetLastError(), "leaf launch");
+  B.copy_back(s);
+  cuda_check(cudaStreamSynchronize(s), "synchronize");
+}
+
+// gemm entry (gemm.cpp:155-216).
+template <typename T>
+void gemm_entry(T alpha, int32_t ta_c, const rectri_cu_view& Av, int32_t tb_c,
+                const rectri_cu_view& Bv, T beta, const rectri_cu_view& Cv,
+                const rectri_cu_backend* cbe) {
+  validate_view(Av, "A");
+  validate_view(Bv, "B");
+  validate_view(Cv, "C");
+  const BackendInfo be = validate_backend(cbe);
+  if (ta_c < 0 || ta_c > 2 || tb_c < 0 || tb_c > 2) fail(RECTRI_CU_CONFIG, "trans out of range");
+  const bool ta = ta_c != RECTRI_CU_NOTRANS, tb = tb_c != RECTRI_CU_NOTRANS;
+  const i64 M = Cv.rows, N = Cv.cols;
+  const i64 Kd = ta ? Av.rows : Av.cols;
+  const i64 a_rows = ta ? Av.cols : Av.rows;
+  const i64 b_rows = tb ? Bv.cols : Bv.rows;
+  const i64 b_cols = tb ? Bv.rows : Bv.cols;
+  if (a_rows != M || b_rows != Kd || b_cols != N)
+    fail(RECTRI_CU_SHAPE, "gemm: op(A) is %lldx%lld, op(B) is %lldx%lld, C is %lldx%lld",
+         (long long)a_rows, (long long)Kd, (long long)b_rows, (long long)b_cols, (long long)M,
+         (long long)N);
+  if (overlaps(Cv, Av) || overlaps(Cv, Bv)) fail(RECTRI_CU_ALIAS, "gemm: C overlaps an input view");
+  if (M == 0 || N == 0) return;
+  DeviceGuard guard(be.device);
+  cudaStream_t s = be.stream;
+  Staged<const T> A(Av, s);
+  Staged<const T> B(Bv, s);
+  Staged<T> C(Cv, s);
+  enqueue_gemm<T>(alpha, ta, A.view, tb, B.view, beta, C.view, s);
+  cuda_check(cudaGetLastError(), "gemm launch");
+  C.copy_back(s);
+  cuda_check(cudaStreamSynchronize(s), "synchronize");
+}
+
+template <typename T>
+void scale_entry(T alpha, const rectri_cu_view& Bv, const rectri_cu_backend* cbe) {
+  validate_view(Bv, "B");
+  const BackendInfo be = validate_backend(cbe);
+  if (alpha == T(1) || view_empty(Bv)) return;  // gemm.cpp:219
+  DeviceGuard guard(be.device);
+  cudaStream_t s = be.stream;
+  Staged<T> B(Bv, s);
+  K<T>::scale(B.view.p, B.view.ld, B.view.rows, B.view.cols, alpha, s);
+  cuda_check(cudaGetLastError(), "scale launch");
+  B.copy_back(s);
+  cuda_check(cudaStreamSynchronize(s), "synchronize");
+}
+
+}  // namespace
+}  // namespace rectri_cu
+
+using namespace rectri_cu;
+
+extern "C" {
+
+int rectri_cu_rec_trmm_f64(const rectri_cu_spec* spec, rectri_cu_view A, rectri_cu_view B,
+                           int64_t threshold, const rectri_cu_backend* backend,
+                           rectri_cu_event_fn sink, void* sink_user) {
+  return guarded([&] { rec_entry<double>(kTrmm, spec, A, B, threshold, backend, sink, sink_user); },
+                 nullptr);
+}
+int rectri_cu_rec_trmm_f32(const rectri_cu_spec* spec, rectri_cu_view A, rectri_cu_view B,
+                           int64_t threshold, const rectri_cu_backend* backend,
+                           rectri_cu_event_fn sink, void* sink_user) {
+  return guarded([&] { rec_entry<float>(kTrmm, spec, A, B, threshold, backend, sink, sink_user); },
+                 nullptr);
+}
+int rectri_cu_rec_trsm_f64(const rectri_cu_spec* spec, rectri_cu_view A, rectri_cu_view B,
+                           int64_t threshold, const rectri_cu_backend* backend,
+                           rectri_cu_event_fn sink, void* sink_user, int64_t* singular_row) {
+  return guarded([&] { rec_entry<double>(kTrsm, spec, A, B, threshold, backend, sink, sink_user); },
+                 singular_row);
+}
+int rectri_cu_rec_trsm_f32(const rectri_cu_spec* spec, rectri_cu_view A, rectri_cu_view B,
+                           int64_t threshold, const rectri_cu_backend* backend,
+                           rectri_cu_event_fn sink, void* sink_user, int64_t* singular_row) {
+  return guarded([&] { rec_entry<float>(kTrsm, spec, A, B, threshold, backend, sink, sink_user); },
+                 singular_row);
+}
+
+int rectri_cu_trmm_base_f64(const rectri_cu_spec* spec, rectri_cu_view A, rectri_cu_view B,
+                            int64_t tile_limit, const rectri_cu_backend* backend) {
+  return guarded([&] { base_entry<double>(kTrmm, spec, A, B, tile_limit, backend); }, nullptr);
+}
+int rectri_cu_trmm_base_f32(const rectri_cu_spec* spec, rectri_cu_view A, rectri_cu_view B,
+                            int64_t tile_limit, const rectri_cu_backend* backend) {
+  return guarded([&] { base_entry<float>(kTrmm, spec, A, B, tile_limit, backend); }, nullptr);
+}
+int rectri_cu_trsm_base_f64(const rectri_cu_spec* spec, rectri_cu_view A, rectri_cu_view B,
+                            int64_t tile_limit, const rectri_cu_backend* backend,
+                            int64_t* singular_row) {
+  return guarded([&] { base_entry<double>(kTrsm, spec, A, B, tile_limit, backend); }, singular_row);
+}
+int rectri_cu_trsm_base_f32(const rectri_cu_spec* spec, rectri_cu_view A, rectri_cu_view B,
+                            int64_t tile_limit, const rectri_cu_backend* backend,
+                            int64_t* singular_row) {
+  return guarded([&] { base_entry<float>(kTrsm, spec, A, B, tile_limit, backend); }, singular_row);
+}
+
+int rectri_cu_gemm_f64(double alpha, int32_t trans_a, rectri_cu_view A, int32_t trans_b,
+                       rectri_cu_view B, double beta, rectri_cu_view C,
+                       const rectri_cu_backend* backend) {
+  return guarded([&] { gemm_entry<double>(alpha, trans_a, A, trans_b, B, beta, C, backend); },
+                 nullptr);
+}
+int rectri_cu_gemm_f32(float alpha, int32_t trans_a, rectri_cu_view A, int32_t trans_b,
+                       rectri_cu_view B, float beta, rectri_cu_view C,
+                       const rectri_cu_backend* backend) {
+  return guarded([&] { gemm_entry<float>(alpha, trans_a, A, trans_b, B, beta, C, backend); },
+                 nullptr);
+}
+
+int rectri_cu_scale_f64(double alpha, rectri_cu_view B, const rectri_cu_backend* backend) {
+  return guarded([&] { scale_entry<double>(alpha, B, backend); }, nullptr);
+}
+int rectri_cu_scale_f32(float alpha, rectri_cu_view B, const rectri_cu_backend* backend) {
+  return guarded([&] { scale_entry<float>(alpha, B, backend); }, nullptr);
+}
+
+int rectri_cu_schema_for(int32_t op, const rectri_cu_spec* spec, double out[8]) {
+  return guarded(
+      [&] {
+        const Spec s = validate_spec(spec);
+        const Schema sc = schema_for(op == 1 ? kTrsm : kTrmm, s.side, s.uplo, s.trans);
+        out[0] = sc.first_a22;
+        out[1] = sc.off_trans;
+        out[2] = sc.off_on_left;
+        out[3] = sc.read_b2;
+        out[4] = sc.write_b2;
+        out[5] = sc.sign;
+        out[6] = sc.carries_alpha;
+        out[7] = !sc.first_a22;
+      },
+      nullptr);
+}
+
+int rectri_cu_sync(void* stream, int64_t* singular_row) {
+  return guarded(
+      [&] {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        cuda_check(cudaStreamSynchronize(s), "synchronize");
+        std::vector<std::shared_ptr<GraphEntry>> pend;
+        {
+          std::lock_guard<std::mutex> lock(g_mu);
+          auto range = g_pending.equal_range(s);
+          for (auto it = range.first; it != range.second; ++it) pend.push_back(it->second);
+          g_pending.erase(s);
+        }
+        for (const auto& g : pend) {
+          const i64 r = first_singular(*g);
+          if (r >= 0) {
+            Fail f{RECTRI_CU_SINGULAR,
+                   "singular triangular matrix: zero diagonal at row " + std::to_string(r)};
+            f.index = r;
+            throw f;
+          }
+        }
+      },
+      singular_row);
+}
+
+const char* rectri_cu_last_error(void) { return g_last_error.c_str(); }
+
+int64_t rectri_cu_launch_count(void) { return launch_counter(); }
+
+void rectri_cu_clear_graph_cache(void) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_pending.clear();
+  g_cache.clear();
+}
+
+int rectri_cu_abi_version(void) { return RECTRI_CU_ABI_VERSION; }
+
+int rectri_cu_fill_uniform(int32_t dtype, rectri_cu_view B, int64_t col0, int64_t global_rows,
+                           uint64_t seed, const rectri_cu_backend* backend) {
+  return guarded(
+      [&] {
+        validate_view(B, "B");
+        const BackendInfo be = validate_backend(backend);
+        if (view_empty(B)) return;
+        if (!is_device_memory(B.origin)) fail(RECTRI_CU_CONFIG, "fill_uniform needs device memory");
+        DeviceGuard guard(be.device);
+        if (dtype == 1) {
+          DView<double> v = dview_of<double>(B);
+          launch_fill_uniform_f64(v.p, v.ld, v.rows, v.cols, col0, global_rows, seed, be.stream);
+        } else {
+          DView<float> v = dview_of<float>(B);
+          launch_fill_uniform_f32(v.p, v.ld, v.rows, v.cols, col0, global_rows, seed, be.stream);
+        }
+        cuda_check(cudaGetLastError(), "fill launch");
+        if (!(be.flags & RECTRI_CU_ASYNC)) cuda_check(cudaStreamSynchronize(be.stream), "synchronize");
+      },
+      nullptr);
+}
+
+int rectri_cu_make_dominant(int32_t dtype, rectri_cu_view A, int32_t uplo,
+                            const rectri_cu_backend* backend) {
+  return guarded(
+      [&] {
+        validate_view(A, "A");
+        const BackendInfo be = validate_backend(backend);
+        if (A.rows != A.cols) fail(RECTRI_CU_SHAPE, "A must be square");
+        if (view_empty(A)) return;
+        if (!is_device_memory(A.origin)) fail(RECTRI_CU_CONFIG, "make_dominant needs device memory");
+        DeviceGuard guard(be.device);
+        if (dtype == 1) {
+          DView<double> v = dview_of<double>(A);
+          launch_make_dominant_f64(v.p, v.ld, v.rows, uplo, be.stream);
+        } else {
+          DView<float> v = dview_of<float>(A);
+          launch_make_dominant_f32(v.p, v.ld, v.rows, uplo, be.stream);
+        }
+        cuda_check(cudaGetLastError(), "dominant launch");
+        if (!(be.flags & RECTRI_CU_ASYNC)) cuda_check(cudaStreamSynchronize(be.stream), "synchronize");
+      },
+      nullptr);
+}
+
+double rectri_cu_probe_peak(int32_t kind) { return probe_peak_tflops(kind); }
+
+void rectri_cu_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_prof.on = on != 0;
+}
+
+int rectri_cu_profile_read(double ms[4], int64_t launches[4], double flops[4]) {
+  return guarded(
+      [&] {
+        for (int k = 0; k < 4; ++k) {
+          ms[k] = 0.0;
+          launches[k] = 0;
+          flops[k] = 0.0;
+        }
+        std::vector<ProfRec> recs;
+        {
+          std::lock_guard<std::mutex> lock(g_mu);
+          recs.swap(g_prof.recs);
+        }
+        for (ProfRec& r : recs) {
+          cuda_check(cudaEventSynchronize(r.b), "profile sync");
+          float t = 0.f;
+          cuda_check(cudaEventElapsedTime(&t, r.a, r.b), "profile elapsed");
+          if (r.kind >= 0 && r.kind < 4) {
+            ms[r.kind] += t;
+            launches[r.kind] += 1;
+            flops[r.kind] += r.flops;
+          }
+          cudaEventDestroy(r.a);
+          cudaEventDestroy(r.b);
+        }
+      },
+      nullptr);
+}
+
+}  // extern "C"

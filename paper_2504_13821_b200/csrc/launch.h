@@ -1,0 +1,75 @@
+// launch.h -- host-side launchers of the sm_100a kernels (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rectri_cu {
+
+using i64 = int64_t;
+
+// C[M x N] <- alpha * op(A)[M x K] * op(B)[K x N] + beta * C, column-major.
+// beta == 0 never reads C.  The per-element reduction order is k-ascending
+// and independent of the tile configuration chosen (so results do not depend
+// on N, which is what makes RHS sharding bitwise-stable).
+template <typename T>
+struct GemmParams {
+  i64 M, N, K;
+  T alpha, beta;
+  const T* A;
+  i64 lda;
+  const T* B;
+  i64 ldb;
+  T* C;
+  i64 ldc;
+};
+
+// Leaf (base-kernel) problem in the reference's Left form on a virtual lower
+// factor L' (base_kernels.cpp:35-89): element r of right-hand side c is
+// B(pi(r), c) (Left) or B(c, pi(r)) (Right, `right` = 1), pi(r) = n-1-r when
+// `reflected`; L'(r, j) = A(R(r), R(j)) or, when `swapped`, A(R(j), R(r)),
+// with R the same reflection.  Unit diag never reads A(r, r).
+template <typename T>
+struct LeafParams {
+  int n;  // tile order, <= kLeafMax
+  i64 nrhs;
+  const T* A;
+  i64 lda;
+  T* B;
+  i64 ldb;
+  int right;
+  int reflected;
+  int swapped;
+  int unit;
+  int trsm;  // 1: solve, 0: multiply
+  T alpha;
+};
+
+constexpr int kLeafMax = 256;
+
+void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s);
+void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s);
+void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s);
+void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s);
+
+// B[rows x cols] (ld) <- alpha * B.
+void launch_scale_f64(double* B, i64 ld, i64 rows, i64 cols, double alpha, cudaStream_t s);
+void launch_scale_f32(float* B, i64 ld, i64 rows, i64 cols, float alpha, cudaStream_t s);
+// flags[r] = (A(r, r) == 0) for r < n.
+void launch_diag_zero_scan_f64(const double* A, i64 lda, i64 n, uint8_t* flags, cudaStream_t s);
+void launch_diag_zero_scan_f32(const float* A, i64 lda, i64 n, uint8_t* flags, cudaStream_t s);
+
+// Synthetic inputs: uniform [-1, 1) keyed by the global element index
+// (col0 + c) * global_rows + r; diagonal := off-diagonal |row sum| + 1.
+void launch_fill_uniform_f64(double* B, i64 ld, i64 rows, i64 cols, i64 col0, i64 grows,
+                             uint64_t seed, cudaStream_t s);
+void launch_fill_uniform_f32(float* B, i64 ld, i64 rows, i64 cols, i64 col0, i64 grows,
+                             uint64_t seed, cudaStream_t s);
+void launch_make_dominant_f64(double* A, i64 lda, i64 n, int upper, cudaStream_t s);
+void launch_make_dominant_f32(float* A, i64 lda, i64 n, int upper, cudaStream_t s);
+double probe_peak_tflops(int kind);
+
+// Number of kernel launches issued (incremented by each launcher).
+i64& launch_counter();
+
+}  // namespace rectri_cu
