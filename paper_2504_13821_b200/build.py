@@ -85,6 +85,26 @@ def build(verbose: bool = False) -> Path:
     return LIB
 
 
+EXAMPLE_SRC = ROOT / "tests" / "cpp" / "dropin_example.cpp"
+EXAMPLE_BIN = ROOT / "tests" / "cpp" / "build" / "dropin_example"
+
+
+def build_dropin_example() -> Path:
+    """Compiles reference-style C++ user code against include/rectri/ (the
+    drop-in headers) and links it to the in-tree library."""
+    EXAMPLE_BIN.parent.mkdir(parents=True, exist_ok=True)
+    deps = [EXAMPLE_SRC, LIB, ROOT / "include" / "rectri_b200.hpp", ROOT / "include" / "rectri_cu.h"]
+    if _stale(EXAMPLE_BIN, deps):
+        cmd = [os.environ.get("CXX", "g++"), "-std=c++17", "-O2", "-Wall", f"-I{ROOT / 'include'}",
+               str(EXAMPLE_SRC), f"-L{LIB.parent}", "-lrectri_cu", "-Wl,-rpath,$ORIGIN/../../../paper_2504_13821_b200/lib",
+               "-o", str(EXAMPLE_BIN)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"drop-in example failed to build:\n{r.stderr}")
+    return EXAMPLE_BIN
+
+
 if __name__ == "__main__":
     build(verbose=True)
+    build_dropin_example()
     sys.exit(0)

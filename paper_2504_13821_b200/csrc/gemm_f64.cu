@@ -4,13 +4,20 @@
 // src/gemm_kernels_avx2.cpp:13-67) for the off-diagonal updates
 // B_dst += coeff * op(A_off) * B_src (Left) / B_src * op(A_off) (Right),
 // recursion.cpp:134-143.  tcgen05 has no f64 kind, so the tensor path is
-// mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4 (measured 36.9 TF/s peak on B200,
-// profiles/r01_microbench_peaks.jsonl).
+// mma.sync.m16n8k4.f64 -> 2x SASS DMMA.8x8x4 (36.9 TF/s measured peak on
+// B200, profiles/r01_microbench_peaks.jsonl).
 //
-// Structure: CTA tile BM x BN x 16, STAGES-deep cp.async (LDGSTS) ring in
-// shared memory (swizzled, conflict-free fragment reads), warps of WM x WN
-// sub-tiles issuing DMMA from register fragments, fused epilogue
-// C = fma(alpha, acc, beta * C).
+// Structure: CTA tile BM x BN x 16; a STAGES-deep cp.async (LDGSTS) ring in
+// shared memory with an XOR swizzle that makes every fragment read
+// conflict-free; warps own WM x WN sub-tiles and issue DMMA from register
+// fragments that are double-buffered across the four k-steps of a tile; one
+// __syncthreads per k-tile, placed before the last k-step so the next tile's
+// first fragments load underneath the last MMAs; fused epilogue
+// C = fma(alpha, acc, beta * C) (beta == 0 never reads C).
+//
+// Determinism: every configuration accumulates each element over k in the
+// same order (16-wide k-tiles, four m16n8k4 steps each), so the result does
+// not depend on the tile shape chosen for a given M, N.
 #include "common.cuh"
 #include "launch.h"
 
@@ -19,80 +26,76 @@ namespace {
 
 constexpr int kBK = 16;
 
-// Outer-contiguous operand tile ("MC"): element (o, k) at X[o + k * ld];
-// shared rows are k (kBK rows of BO doubles).
-template <int BO, int NT, int VEC>
-__device__ __forceinline__ void load_tile_mc(double* s, const double* X, i64 ld, i64 o0, i64 O,
-                                             i64 k0, i64 K) {
-  if constexpr (VEC == 2) {
-    constexpr int CPR = BO / 2;
-    constexpr int TOTAL = kBK * CPR;
-#pragma unroll
-    for (int q = threadIdx.x; q < TOTAL; q += NT) {
-      const int k = q / CPR, oc = q % CPR;
-      const i64 go = o0 + 2 * oc, gk = k0 + k;
-      int bytes = 0;
-      const double* src = X;
-      if (gk < K && go < O) {
-        bytes = (O - go) >= 2 ? 16 : 8;
-        src = X + go + gk * ld;
-      }
-      cp_async16(s + k * BO + ((oc ^ ((k & 3) << 1)) << 1), src, bytes);
-    }
-  } else {
-    constexpr int TOTAL = kBK * BO;
-#pragma unroll 4
-    for (int q = threadIdx.x; q < TOTAL; q += NT) {
-      const int k = q / BO, o = q % BO;
-      const i64 go = o0 + o, gk = k0 + k;
-      const bool ok = gk < K && go < O;
-      cp_async8(s + swz64(k, o, BO), ok ? X + go + gk * ld : X, ok ? 8 : 0);
-    }
-  }
+__device__ __forceinline__ void dmma1684(double (&c)[4], double a0, double a1, double b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b));
 }
 
-// k-contiguous operand tile ("KC"): element (o, k) at X[k + o * ld]; shared
-// rows are o (BO rows of kBK doubles).
-template <int BO, int NT, int VEC>
-__device__ __forceinline__ void load_tile_kc(double* s, const double* X, i64 ld, i64 o0, i64 O,
-                                             i64 k0, i64 K) {
-  if constexpr (VEC == 2) {
-    constexpr int TOTAL = BO * (kBK / 2);
+// Per-thread loader of one operand tile.  Shared rows hold CPR chunks of
+// VEC doubles; thread q copies the chunks q, q + NT, ... so its chunk column
+// is fixed and its row advances by NT / CPR per iteration.
+//   MC: outer-contiguous source, element (o, k) at X[o + k*ld]; rows = k.
+//   KC: k-contiguous source, element (o, k) at X[k + o*ld]; rows = o.
+// Out-of-range elements are zero-filled by the cp.async src-size operand.
+template <int BO, int NT, int VEC, bool KC>
+struct TileLoader {
+  static constexpr int WIDTH = KC ? kBK : BO;  // shared row width (doubles)
+  static constexpr int CPR = WIDTH / VEC;
+  static constexpr int ROWS = KC ? BO : kBK;
+  static constexpr int IT = CPR * ROWS / NT;
+  static constexpr int ROW_STEP = NT / CPR;
+  static_assert(NT % CPR == 0 && (CPR * ROWS) % NT == 0, "loader trip count");
+
+  const double* base;  // X at the tile's outer origin o0
+  i64 ld;
+  int row0, col;       // thread's first shared row, its chunk column (elements)
+  int o_lim, k_lim;    // outer extent left from o0, and K
+
+  __device__ void init(const double* X, i64 ld_, i64 o0, i64 O, i64 K) {
+    ld = ld_;
+    row0 = threadIdx.x / CPR;
+    col = (threadIdx.x % CPR) * VEC;
+    o_lim = static_cast<int>(O - o0 < (1 << 30) ? O - o0 : (1 << 30));
+    k_lim = static_cast<int>(K < (1 << 30) ? K : (1 << 30));
+    base = KC ? X + o0 * ld : X + o0;
+  }
+
+  __device__ __forceinline__ void load(uint32_t stage, i64 kt) const {
+    const int k0 = static_cast<int>(kt * kBK);
 #pragma unroll
-    for (int q = threadIdx.x; q < TOTAL; q += NT) {
-      const int o = q >> 3, kc = q & 7;
-      const i64 go = o0 + o, gk = k0 + 2 * kc;
-      int bytes = 0;
-      const double* src = X;
-      if (go < O && gk < K) {
-        bytes = (K - gk) >= 2 ? 16 : 8;
-        src = X + gk + go * ld;
-      }
-      cp_async16(s + o * kBK + ((kc ^ ((o & 3) << 1)) << 1), src, bytes);
-    }
-  } else {
-    constexpr int TOTAL = BO * kBK;
-#pragma unroll 4
-    for (int q = threadIdx.x; q < TOTAL; q += NT) {
-      const int o = q >> 4, k = q & 15;
-      const i64 go = o0 + o, gk = k0 + k;
-      const bool ok = go < O && gk < K;
-      cp_async8(s + swz64(o, k, kBK), ok ? X + gk + go * ld : X, ok ? 8 : 0);
+    for (int it = 0; it < IT; ++it) {
+      const int row = row0 + it * ROW_STEP;
+      const int o = KC ? row : col;
+      const int k = k0 + (KC ? col : row);
+      const int rem = KC ? k_lim - k : o_lim - o;
+      const bool in = KC ? o < o_lim : k < k_lim;
+      const int bytes = in ? (rem >= VEC ? VEC * 8 : (rem > 0 ? rem * 8 : 0)) : 0;
+      const double* g = bytes ? (KC ? base + o * ld + k : base + o + static_cast<i64>(k) * ld) : base;
+      const uint32_t dst = stage + 8u * static_cast<uint32_t>(swz64(row, col, WIDTH));
+      if constexpr (VEC == 2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(g), "r"(bytes));
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(g), "r"(bytes));
     }
   }
-}
+};
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool TA, bool TB, int VEC>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
     dgemm_dmma_kernel(const GemmParams<double> p) {
   constexpr int NT = WARPS_M * WARPS_N * 32;
   constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
-  constexpr int TM = WM / 8, TN = WN / 8;
-  static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile");
+  constexpr int TM = WM / 16, TN = WN / 8;
+  constexpr int KK = kBK / 4;
+  static_assert(WM % 16 == 0 && WN % 8 == 0, "warp tile");
+  constexpr uint32_t A_STAGE = BM * kBK * 8, B_STAGE = BN * kBK * 8;
 
   extern __shared__ __align__(128) double smem[];
-  double* sA = smem;
-  double* sB = smem + STAGES * BM * kBK;
+  const uint32_t sA = smem_u32(smem);
+  const uint32_t sB = sA + STAGES * A_STAGE;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -101,78 +104,122 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
   const i64 n0 = static_cast<i64>(blockIdx.y) * BN;
   const i64 KT = ceil_div(p.K, kBK);
 
-  auto load_stage = [&](int stage, i64 kt) {
-    const i64 k0 = kt * kBK;
-    double* a = sA + stage * BM * kBK;
-    double* b = sB + stage * BN * kBK;
-    if constexpr (TA) load_tile_kc<BM, NT, VEC>(a, p.A, p.lda, m0, p.M, k0, p.K);
-    else load_tile_mc<BM, NT, VEC>(a, p.A, p.lda, m0, p.M, k0, p.K);
-    if constexpr (TB) load_tile_mc<BN, NT, VEC>(b, p.B, p.ldb, n0, p.N, k0, p.K);
-    else load_tile_kc<BN, NT, VEC>(b, p.B, p.ldb, n0, p.N, k0, p.K);
-  };
+  TileLoader<BM, NT, VEC, TA> la;
+  TileLoader<BN, NT, VEC, !TB> lb;
+  la.init(p.A, p.lda, m0, p.M, p.K);
+  lb.init(p.B, p.ldb, n0, p.N, p.K);
 
-  double acc[TM][TN][2];
+  // Per-thread fragment offsets (bytes, within a stage) for k-step 0; later
+  // k-steps add a constant (the swizzle depends on row & 3 only, and k-steps
+  // move the k index by 4 rows in k-major layouts).
+  uint32_t a_off[TM][2], b_off[TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int h = 0; h < 2; ++h) {
+      const int m = wm0 + 16 * i + 8 * h + g;
+      a_off[i][h] = 8u * static_cast<uint32_t>(TA ? swz64(m, t, kBK) : swz64(t, m, BM));
+    }
+#pragma unroll
+  for (int j = 0; j < TN; ++j) {
+    const int n = wn0 + 8 * j + g;
+    b_off[j] = 8u * static_cast<uint32_t>(TB ? swz64(t, n, BN) : swz64(n, t, kBK));
+  }
+  // k-major layouts: a k-step moves 4 rows and keeps (row & 3), hence the
+  // swizzle; k-contiguous layouts recompute the swizzled column.
+  auto a_addr = [&](uint32_t stage, int i, int h, int kk) -> uint32_t {
+    if constexpr (!TA) return stage + a_off[i][h] + static_cast<uint32_t>(kk * 4 * BM * 8);
+    const int m = wm0 + 16 * i + 8 * h + g;
+    return stage + 8u * static_cast<uint32_t>(swz64(m, kk * 4 + t, kBK));
+  };
+  auto b_addr = [&](uint32_t stage, int j, int kk) -> uint32_t {
+    if constexpr (TB) return stage + b_off[j] + static_cast<uint32_t>(kk * 4 * BN * 8);
+    const int n = wn0 + 8 * j + g;
+    return stage + 8u * static_cast<uint32_t>(swz64(n, kk * 4 + t, kBK));
+  };
+
+  double af[2][TM][2], bf[2][TN];
+  auto load_frags = [&](int buf, int stage, int kk) {
+    const uint32_t as = sA + stage * A_STAGE, bs = sB + stage * B_STAGE;
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(af[buf][i][h]) : "r"(a_addr(as, i, h, kk)));
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+      asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(bf[buf][j]) : "r"(b_addr(bs, j, kk)));
+  };
+
+  double acc[TM][TN][4];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(s, s);
+    if (s < KT) {
+      la.load(sA + s * A_STAGE, s);
+      lb.load(sB + s * B_STAGE, s);
+    }
     cp_async_commit();
   }
+  cp_async_wait<STAGES - 2>();
+  __syncthreads();
+  load_frags(0, 0, 0);
 
   for (i64 kt = 0; kt < KT; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
+    {  // refill the stage of tile kt-1 (fully consumed before the last barrier)
       const i64 nk = kt + STAGES - 1;
-      if (nk < KT) load_stage(static_cast<int>(nk % STAGES), nk);
+      if (nk < KT) {
+        const int ws = static_cast<int>(nk % STAGES);
+        la.load(sA + ws * A_STAGE, nk);
+        lb.load(sB + ws * B_STAGE, nk);
+      }
       cp_async_commit();
     }
-    const int st = static_cast<int>(kt % STAGES);
-    const double* a_s = sA + st * BM * kBK;
-    const double* b_s = sB + st * BN * kBK;
+    const int rs = static_cast<int>(kt % STAGES);
 #pragma unroll
-    for (int kk = 0; kk < kBK / 4; ++kk) {
-      const int k = kk * 4 + t;
-      double af[TM], bf[TN];
-#pragma unroll
-      for (int i = 0; i < TM; ++i) {
-        const int m = wm0 + 8 * i + g;
-        af[i] = TA ? a_s[swz64(m, k, kBK)] : a_s[swz64(k, m, BM)];
-      }
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int n = wn0 + 8 * j + g;
-        bf[j] = TB ? b_s[swz64(k, n, BN)] : b_s[swz64(n, k, kBK)];
+    for (int kk = 0; kk < KK; ++kk) {
+      const int cb = kk & 1, nb = cb ^ 1;
+      if (kk < KK - 1) {
+        load_frags(nb, rs, kk + 1);
+      } else {
+        cp_async_wait<STAGES - 2>();  // tile kt+1 has landed (this thread's part)
+        __syncthreads();              // ... and everyone's; stage rs-1 is free
+        if (kt + 1 < KT) load_frags(nb, static_cast<int>((kt + 1) % STAGES), 0);
       }
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < TN; ++j) dmma1684(acc[i][j], af[cb][i][0], af[cb][i][1], bf[cb][j]);
     }
   }
   cp_async_wait<0>();
 
   const bool beta_zero = p.beta == 0.0;
 #pragma unroll
-  for (int i = 0; i < TM; ++i) {
-    const i64 m = m0 + wm0 + 8 * i + g;
-    if (m >= p.M) continue;
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      const i64 n = n0 + wn0 + 8 * j + 2 * t;
+    for (int h = 0; h < 2; ++h) {
+      const i64 m = m0 + wm0 + 16 * i + 8 * h + g;
+      if (m >= p.M) continue;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (n + e < p.N) {
-          double* c = p.C + m + (n + e) * p.ldc;
-          *c = beta_zero ? p.alpha * acc[i][j][e] : fma(p.alpha, acc[i][j][e], p.beta * *c);
+      for (int j = 0; j < TN; ++j) {
+        const i64 n = n0 + wn0 + 8 * j + 2 * t;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (n + e < p.N) {
+            double* c = p.C + m + (n + e) * p.ldc;
+            const double v = acc[i][j][2 * h + e];
+            *c = beta_zero ? p.alpha * v : fma(p.alpha, v, p.beta * *c);
+          }
         }
       }
     }
-  }
 }
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool TA, bool TB, int VEC>
@@ -202,14 +249,26 @@ void dispatch_trans(const GemmParams<double>& p, bool ta, bool tb, bool vec2, cu
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
 
+int g_variant = -1;  // RECTRI_CU_GEMM64 override (tuning / tests)
+
+int variant() {
+  if (g_variant < 0) {
+    const char* e = getenv("RECTRI_CU_GEMM64");
+    g_variant = e ? atoi(e) : 0;
+  }
+  return g_variant;
+}
+
 }  // namespace
 
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
   const bool vec2 = aligned16(p.A) && aligned16(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
   // Tile choice only changes which CTA owns an element, never its k order.
+  const int v = variant();
   if (p.M >= 128 && p.N >= 128) {
-    dispatch_trans<128, 128, 2, 4, 4>(p, ta, tb, vec2, s);
+    if (v == 1) dispatch_trans<128, 128, 4, 4, 4>(p, ta, tb, vec2, s);
+    else dispatch_trans<128, 128, 2, 4, 4>(p, ta, tb, vec2, s);
   } else if (p.N >= 128) {
     dispatch_trans<64, 128, 2, 4, 4>(p, ta, tb, vec2, s);
   } else if (p.M >= 128) {

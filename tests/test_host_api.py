@@ -176,3 +176,13 @@ def test_errors_map_one_to_one():
         raise_for_status(4, "", 17)
     assert e.value.index() == 17
     raise_for_status(0, "")
+
+
+def test_cpp_dropin_compiles_against_reference_style_headers():
+    """Reference-style user code (#include "rectri/recursion.hpp",
+    rec_trsm<float>(spec, a.view(), b.view(), Threshold{..}, Backend::par()))
+    compiles against the drop-in headers and links to librectri_cu.so."""
+    from paper_2504_13821_b200 import build as b
+
+    exe = b.build_dropin_example()
+    assert exe.exists()

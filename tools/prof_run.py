@@ -1,0 +1,46 @@
+"""One-shot workloads for ncu (never a bench number):
+
+    python tools/prof_run.py trsm N M T      one rec_trsm (direct launches)
+    python tools/prof_run.py gemm M N K      one DMMA GEMM update C -= A*B (NN)
+    python tools/prof_run.py leaf NB M       one trsm_base leaf (NB x M)
+"""
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2504_13821_b200 as rc  # noqa: E402
+from paper_2504_13821_b200 import NO_GRAPH, Backend, MatrixBuffer, Threshold, Trans, TriangularSpec  # noqa: E402
+
+kind = sys.argv[1]
+args = [int(x) for x in sys.argv[2:]]
+f64 = torch.float64
+be = Backend.cuda(flags=NO_GRAPH)
+if kind in ("trsm", "trmm"):
+    n, m, t = args
+    A = MatrixBuffer(n, n, f64, "cuda")
+    rc.fill_uniform(A.view(), seed=1)
+    rc.make_dominant(A.view())
+    B = MatrixBuffer(n, m, f64, "cuda")
+    rc.fill_uniform(B.view(), seed=2)
+    fn = rc.rec_trsm if kind == "trsm" else rc.rec_trmm
+    fn(TriangularSpec(), A.cview(), B.view(), Threshold(t), be)
+elif kind == "gemm":
+    M, N, K = args
+    A = MatrixBuffer(M, K, f64, "cuda")
+    B = MatrixBuffer(K, N, f64, "cuda")
+    C = MatrixBuffer(M, N, f64, "cuda")
+    for i, x in enumerate((A, B, C)):
+        rc.fill_uniform(x.view(), seed=i)
+    rc.gemm(-1.0, Trans.NoTrans, A.cview(), Trans.NoTrans, B.cview(), 1.0, C.view(), be)
+elif kind == "leaf":
+    nb, m = args
+    A = MatrixBuffer(nb, nb, f64, "cuda")
+    rc.fill_uniform(A.view(), seed=1)
+    rc.make_dominant(A.view())
+    B = MatrixBuffer(nb, m, f64, "cuda")
+    rc.fill_uniform(B.view(), seed=2)
+    rc.trsm_base(TriangularSpec(), A.cview(), B.view(), nb, be)
+torch.cuda.synchronize()
+print("done", kind, args)
