@@ -1,262 +1,45 @@
-// gemm_f64.cu -- fp64 GEMM update for the recursion on the sm_100a DMMA path.
+// gemm_f64.cu -- configuration choice for the fp64 DMMA GEMM update.
 //
-// Replaces the reference's blocked CPU GEMM (src/gemm.cpp:17-216, microkernel
-// src/gemm_kernels_avx2.cpp:13-67) for the off-diagonal updates
-// B_dst += coeff * op(A_off) * B_src (Left) / B_src * op(A_off) (Right),
-// recursion.cpp:134-143.  tcgen05 has no f64 kind, so the tensor path is
-// mma.sync.m16n8k4.f64 -> 2x SASS DMMA.8x8x4 (36.9 TF/s measured peak on
-// B200, profiles/r01_microbench_peaks.jsonl).
-//
-// Structure: CTA tile BM x BN x 16; a STAGES-deep cp.async (LDGSTS) ring in
-// shared memory with an XOR swizzle that makes every fragment read
-// conflict-free; warps own WM x WN sub-tiles and issue DMMA from register
-// fragments that are double-buffered across the four k-steps of a tile; one
-// __syncthreads per k-tile, placed before the last k-step so the next tile's
-// first fragments load underneath the last MMAs; fused epilogue
-// C = fma(alpha, acc, beta * C) (beta == 0 never reads C).
-//
-// Determinism: every configuration accumulates each element over k in the
-// same order (16-wide k-tiles, four m16n8k4 steps each), so the result does
-// not depend on the tile shape chosen for a given M, N.
-#include "common.cuh"
-#include "launch.h"
+// The kernel (gemm_f64_kernel.cuh) is instantiated per tile configuration in
+// gemm_f64_cfg*.cu; this file only picks one per call.  Every configuration
+// accumulates each output element over k in the same order, so the choice
+// (which may depend on M, N, K) never changes a result bit -- the property
+// the RHS-sharding invariant (P-GPU == 1-GPU) rests on.  Different BK values
+// share that order: a k-tile of 32 is two k-tiles of 16 back to back.
+#include <cstdlib>
+
+#include "gemm_f64_kernel.cuh"
 
 namespace rectri_cu {
 namespace {
 
-constexpr int kBK = 16;
-
-__device__ __forceinline__ void dmma1684(double (&c)[4], double a0, double a1, double b) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
-      "{%0,%1,%2,%3};\n"
-      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
-      : "d"(a0), "d"(a1), "d"(b));
-}
-
-// Per-thread loader of one operand tile.  Shared rows hold CPR chunks of
-// VEC doubles; thread q copies the chunks q, q + NT, ... so its chunk column
-// is fixed and its row advances by NT / CPR per iteration.
-//   MC: outer-contiguous source, element (o, k) at X[o + k*ld]; rows = k.
-//   KC: k-contiguous source, element (o, k) at X[k + o*ld]; rows = o.
-// Out-of-range elements are zero-filled by the cp.async src-size operand.
-template <int BO, int NT, int VEC, bool KC>
-struct TileLoader {
-  static constexpr int WIDTH = KC ? kBK : BO;  // shared row width (doubles)
-  static constexpr int CPR = WIDTH / VEC;
-  static constexpr int ROWS = KC ? BO : kBK;
-  static constexpr int IT = CPR * ROWS / NT;
-  static constexpr int ROW_STEP = NT / CPR;
-  static_assert(NT % CPR == 0 && (CPR * ROWS) % NT == 0, "loader trip count");
-
-  const double* base;  // X at the tile's outer origin o0
-  i64 ld;
-  int row0, col;       // thread's first shared row, its chunk column (elements)
-  int o_lim, k_lim;    // outer extent left from o0, and K
-
-  __device__ void init(const double* X, i64 ld_, i64 o0, i64 O, i64 K) {
-    ld = ld_;
-    row0 = threadIdx.x / CPR;
-    col = (threadIdx.x % CPR) * VEC;
-    o_lim = static_cast<int>(O - o0 < (1 << 30) ? O - o0 : (1 << 30));
-    k_lim = static_cast<int>(K < (1 << 30) ? K : (1 << 30));
-    base = KC ? X + o0 * ld : X + o0;
-  }
-
-  __device__ __forceinline__ void load(uint32_t stage, i64 kt) const {
-    const int k0 = static_cast<int>(kt * kBK);
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int row = row0 + it * ROW_STEP;
-      const int o = KC ? row : col;
-      const int k = k0 + (KC ? col : row);
-      const int rem = KC ? k_lim - k : o_lim - o;
-      const bool in = KC ? o < o_lim : k < k_lim;
-      const int bytes = in ? (rem >= VEC ? VEC * 8 : (rem > 0 ? rem * 8 : 0)) : 0;
-      const double* g = bytes ? (KC ? base + o * ld + k : base + o + static_cast<i64>(k) * ld) : base;
-      const uint32_t dst = stage + 8u * static_cast<uint32_t>(swz64(row, col, WIDTH));
-      if constexpr (VEC == 2)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(g), "r"(bytes));
-      else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(g), "r"(bytes));
-    }
-  }
-};
-
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool TA, bool TB, int VEC>
-__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
-    dgemm_dmma_kernel(const GemmParams<double> p) {
-  constexpr int NT = WARPS_M * WARPS_N * 32;
-  constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
-  constexpr int TM = WM / 16, TN = WN / 8;
-  constexpr int KK = kBK / 4;
-  static_assert(WM % 16 == 0 && WN % 8 == 0, "warp tile");
-  constexpr uint32_t A_STAGE = BM * kBK * 8, B_STAGE = BN * kBK * 8;
-
-  extern __shared__ __align__(128) double smem[];
-  const uint32_t sA = smem_u32(smem);
-  const uint32_t sB = sA + STAGES * A_STAGE;
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm0 = (warp % WARPS_M) * WM, wn0 = (warp / WARPS_M) * WN;
-  const i64 m0 = static_cast<i64>(blockIdx.x) * BM;
-  const i64 n0 = static_cast<i64>(blockIdx.y) * BN;
-  const i64 KT = ceil_div(p.K, kBK);
-
-  TileLoader<BM, NT, VEC, TA> la;
-  TileLoader<BN, NT, VEC, !TB> lb;
-  la.init(p.A, p.lda, m0, p.M, p.K);
-  lb.init(p.B, p.ldb, n0, p.N, p.K);
-
-  // Per-thread fragment offsets (bytes, within a stage) for k-step 0; later
-  // k-steps add a constant (the swizzle depends on row & 3 only, and k-steps
-  // move the k index by 4 rows in k-major layouts).
-  uint32_t a_off[TM][2], b_off[TN];
-#pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int m = wm0 + 16 * i + 8 * h + g;
-      a_off[i][h] = 8u * static_cast<uint32_t>(TA ? swz64(m, t, kBK) : swz64(t, m, BM));
-    }
-#pragma unroll
-  for (int j = 0; j < TN; ++j) {
-    const int n = wn0 + 8 * j + g;
-    b_off[j] = 8u * static_cast<uint32_t>(TB ? swz64(t, n, BN) : swz64(n, t, kBK));
-  }
-  // k-major layouts: a k-step moves 4 rows and keeps (row & 3), hence the
-  // swizzle; k-contiguous layouts recompute the swizzled column.
-  auto a_addr = [&](uint32_t stage, int i, int h, int kk) -> uint32_t {
-    if constexpr (!TA) return stage + a_off[i][h] + static_cast<uint32_t>(kk * 4 * BM * 8);
-    const int m = wm0 + 16 * i + 8 * h + g;
-    return stage + 8u * static_cast<uint32_t>(swz64(m, kk * 4 + t, kBK));
-  };
-  auto b_addr = [&](uint32_t stage, int j, int kk) -> uint32_t {
-    if constexpr (TB) return stage + b_off[j] + static_cast<uint32_t>(kk * 4 * BN * 8);
-    const int n = wn0 + 8 * j + g;
-    return stage + 8u * static_cast<uint32_t>(swz64(n, kk * 4 + t, kBK));
-  };
-
-  double af[2][TM][2], bf[2][TN];
-  auto load_frags = [&](int buf, int stage, int kk) {
-    const uint32_t as = sA + stage * A_STAGE, bs = sB + stage * B_STAGE;
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(af[buf][i][h]) : "r"(a_addr(as, i, h, kk)));
-#pragma unroll
-    for (int j = 0; j < TN; ++j)
-      asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(bf[buf][j]) : "r"(b_addr(bs, j, kk)));
-  };
-
-  double acc[TM][TN][4];
-#pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int j = 0; j < TN; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) {
-      la.load(sA + s * A_STAGE, s);
-      lb.load(sB + s * B_STAGE, s);
-    }
-    cp_async_commit();
-  }
-  cp_async_wait<STAGES - 2>();
-  __syncthreads();
-  load_frags(0, 0, 0);
-
-  for (i64 kt = 0; kt < KT; ++kt) {
-    {  // refill the stage of tile kt-1 (fully consumed before the last barrier)
-      const i64 nk = kt + STAGES - 1;
-      if (nk < KT) {
-        const int ws = static_cast<int>(nk % STAGES);
-        la.load(sA + ws * A_STAGE, nk);
-        lb.load(sB + ws * B_STAGE, nk);
-      }
-      cp_async_commit();
-    }
-    const int rs = static_cast<int>(kt % STAGES);
-#pragma unroll
-    for (int kk = 0; kk < KK; ++kk) {
-      const int cb = kk & 1, nb = cb ^ 1;
-      if (kk < KK - 1) {
-        load_frags(nb, rs, kk + 1);
-      } else {
-        cp_async_wait<STAGES - 2>();  // tile kt+1 has landed (this thread's part)
-        __syncthreads();              // ... and everyone's; stage rs-1 is free
-        if (kt + 1 < KT) load_frags(nb, static_cast<int>((kt + 1) % STAGES), 0);
-      }
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) dmma1684(acc[i][j], af[cb][i][0], af[cb][i][1], bf[cb][j]);
-    }
-  }
-  cp_async_wait<0>();
-
-  const bool beta_zero = p.beta == 0.0;
-#pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const i64 m = m0 + wm0 + 16 * i + 8 * h + g;
-      if (m >= p.M) continue;
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const i64 n = n0 + wn0 + 8 * j + 2 * t;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          if (n + e < p.N) {
-            double* c = p.C + m + (n + e) * p.ldc;
-            const double v = acc[i][j][2 * h + e];
-            *c = beta_zero ? p.alpha * v : fma(p.alpha, v, p.beta * *c);
-          }
-        }
-      }
-    }
-}
-
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool TA, bool TB, int VEC>
-void launch_cfg(const GemmParams<double>& p, cudaStream_t s) {
-  auto kern = dgemm_dmma_kernel<BM, BN, WARPS_M, WARPS_N, STAGES, TA, TB, VEC>;
-  constexpr int smem = STAGES * (BM + BN) * kBK * static_cast<int>(sizeof(double));
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
-  kern<<<grid, WARPS_M * WARPS_N * 32, smem, s>>>(p);
-  ++launch_counter();
-}
-
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
-void dispatch_trans(const GemmParams<double>& p, bool ta, bool tb, bool vec2, cudaStream_t s) {
-#define RECTRI_CFG(TA_, TB_)                                                            \
-  if (ta == TA_ && tb == TB_) {                                                         \
-    if (vec2) launch_cfg<BM, BN, WARPS_M, WARPS_N, STAGES, TA_, TB_, 2>(p, s);          \
-    else launch_cfg<BM, BN, WARPS_M, WARPS_N, STAGES, TA_, TB_, 1>(p, s);               \
-    return;                                                                             \
-  }
-  RECTRI_CFG(false, false)
-  RECTRI_CFG(true, false)
-  RECTRI_CFG(false, true)
-  RECTRI_CFG(true, true)
-#undef RECTRI_CFG
-}
-
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
 
-int g_variant = -1;  // RECTRI_CU_GEMM64 override (tuning / tests)
+const DgemmRun kRuns[] = {
+#define RECTRI_ENTRY(ID, BM, BN, BK, WM, WN, ST) dgemm_cfg##ID,
+    RECTRI_DGEMM_CONFIGS(RECTRI_ENTRY)
+#undef RECTRI_ENTRY
+};
+constexpr int kNumCfg = sizeof(kRuns) / sizeof(kRuns[0]);
 
-int variant() {
-  if (g_variant < 0) {
-    const char* e = getenv("RECTRI_CU_GEMM64");
-    g_variant = e ? atoi(e) : 0;
-  }
-  return g_variant;
+int forced_config() {  // RECTRI_CU_GEMM64_CFG=<id> pins one configuration (tuning)
+  static int v = [] {
+    const char* e = getenv("RECTRI_CU_GEMM64_CFG");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+
+int choose(const GemmParams<double>& p) {
+  const int f = forced_config();
+  // A 32-deep k-tile zero-pads a K tail that a 16-deep one would not (a
+  // -0.0 accumulator could turn +0.0), so BK=32 configurations are only
+  // eligible when K % 32 == 0, where both produce identical bits.
+  const bool bk32 = f == 2 || f == 3 || f == 7 || f == 8 || f == 9;
+  if (f >= 0 && f < kNumCfg && (p.K % 32 == 0 || !bk32)) return f;
+  // 64x64 CTAs (4 warps, 3 per SM): measured best at every level shape of
+  // the recursion on B200 (profiles/r01_gemm_cfg_sweep.txt).
+  return 6;
 }
 
 }  // namespace
@@ -264,18 +47,7 @@ int variant() {
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
   const bool vec2 = aligned16(p.A) && aligned16(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
-  // Tile choice only changes which CTA owns an element, never its k order.
-  const int v = variant();
-  if (p.M >= 128 && p.N >= 128) {
-    if (v == 1) dispatch_trans<128, 128, 4, 4, 4>(p, ta, tb, vec2, s);
-    else dispatch_trans<128, 128, 2, 4, 4>(p, ta, tb, vec2, s);
-  } else if (p.N >= 128) {
-    dispatch_trans<64, 128, 2, 4, 4>(p, ta, tb, vec2, s);
-  } else if (p.M >= 128) {
-    dispatch_trans<128, 64, 4, 2, 4>(p, ta, tb, vec2, s);
-  } else {
-    dispatch_trans<64, 64, 2, 2, 4>(p, ta, tb, vec2, s);
-  }
+  kRuns[choose(p)](p, ta, tb, vec2, s);
 }
 
 }  // namespace rectri_cu

@@ -1,0 +1,8 @@
+// fp64 DMMA GEMM, configuration 2: CTA 128x128x32, warps 2x4, 3 stages.
+#include "gemm_f64_kernel.cuh"
+
+namespace rectri_cu {
+void dgemm_cfg2(const GemmParams<double>& p, bool ta, bool tb, bool vec2, cudaStream_t s) {
+  dgemm::Config<128, 128, 32, 2, 4, 3>::run(p, ta, tb, vec2, s);
+}
+}  // namespace rectri_cu

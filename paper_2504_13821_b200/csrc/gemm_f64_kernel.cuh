@@ -1,0 +1,280 @@
+// gemm_f64_kernel.cuh -- fp64 GEMM update for the recursion on the sm_100a DMMA path.
+//
+// Replaces the reference's blocked CPU GEMM (src/gemm.cpp:17-216, microkernel
+// src/gemm_kernels_avx2.cpp:13-67) for the off-diagonal updates
+// B_dst += coeff * op(A_off) * B_src (Left) / B_src * op(A_off) (Right),
+// recursion.cpp:134-143.  tcgen05 has no f64 kind, so the tensor path is
+// mma.sync.m16n8k4.f64 -> 2x SASS DMMA.8x8x4 (36.9 TF/s measured peak on
+// B200, profiles/r01_microbench_peaks.jsonl).
+//
+// Structure: CTA tile BM x BN x 16; a STAGES-deep cp.async (LDGSTS) ring in
+// shared memory with an XOR swizzle that makes every fragment read
+// conflict-free; warps own WM x WN sub-tiles and issue DMMA from register
+// fragments that are double-buffered across the four k-steps of a tile; one
+// __syncthreads per k-tile, placed before the last k-step so the next tile's
+// first fragments load underneath the last MMAs; fused epilogue
+// C = fma(alpha, acc, beta * C) (beta == 0 never reads C).
+//
+// Determinism: every configuration accumulates each element over k in the
+// same order (16-wide k-tiles, four m16n8k4 steps each), so the result does
+// not depend on the tile shape chosen for a given M, N.
+#pragma once
+#include "common.cuh"
+#include "launch.h"
+
+namespace rectri_cu {
+namespace dgemm {
+
+
+__device__ __forceinline__ void dmma1684(double (&c)[4], double a0, double a1, double b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+// Per-thread loader of one operand tile.  Shared rows hold CPR chunks of
+// VEC doubles; thread q copies the chunks q, q + NT, ... so its chunk column
+// is fixed and its row advances by NT / CPR per iteration.
+//   MC: outer-contiguous source, element (o, k) at X[o + k*ld]; rows = k.
+//   KC: k-contiguous source, element (o, k) at X[k + o*ld]; rows = o.
+// Out-of-range elements are zero-filled by the cp.async src-size operand.
+template <int BO, int BK, int NT, int VEC, bool KC>
+struct TileLoader {
+  static constexpr int kBK = BK;
+  static constexpr int WIDTH = KC ? kBK : BO;  // shared row width (doubles)
+  static constexpr int CPR = WIDTH / VEC;
+  static constexpr int ROWS = KC ? BO : kBK;
+  static constexpr int IT = CPR * ROWS / NT;
+  static constexpr int ROW_STEP = NT / CPR;
+  static_assert(NT % CPR == 0 && (CPR * ROWS) % NT == 0, "loader trip count");
+
+  const double* base;  // X at the tile's outer origin o0
+  i64 ld;
+  int row0, col;       // thread's first shared row, its chunk column (elements)
+  int o_lim, k_lim;    // outer extent left from o0, and K
+
+  __device__ void init(const double* X, i64 ld_, i64 o0, i64 O, i64 K) {
+    ld = ld_;
+    row0 = threadIdx.x / CPR;
+    col = (threadIdx.x % CPR) * VEC;
+    o_lim = static_cast<int>(O - o0 < (1 << 30) ? O - o0 : (1 << 30));
+    k_lim = static_cast<int>(K < (1 << 30) ? K : (1 << 30));
+    base = KC ? X + o0 * ld : X + o0;
+  }
+
+  __device__ __forceinline__ void load(uint32_t stage, i64 kt) const {
+    const int k0 = static_cast<int>(kt * kBK);
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int row = row0 + it * ROW_STEP;
+      const int o = KC ? row : col;
+      const int k = k0 + (KC ? col : row);
+      const int rem = KC ? k_lim - k : o_lim - o;
+      const bool in = KC ? o < o_lim : k < k_lim;
+      const int bytes = in ? (rem >= VEC ? VEC * 8 : (rem > 0 ? rem * 8 : 0)) : 0;
+      const double* g = bytes ? (KC ? base + o * ld + k : base + o + static_cast<i64>(k) * ld) : base;
+      const uint32_t dst = stage + 8u * static_cast<uint32_t>(swz64(row, col, WIDTH));
+      if constexpr (VEC == 2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(g), "r"(bytes));
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(g), "r"(bytes));
+    }
+  }
+};
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TA, bool TB, int VEC>
+__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
+    dgemm_dmma_kernel(const GemmParams<double> p) {
+  constexpr int kBK = BK;
+  constexpr int NT = WARPS_M * WARPS_N * 32;
+  constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
+  constexpr int TM = WM / 16, TN = WN / 8;
+  constexpr int KK = kBK / 4;
+  static_assert(WM % 16 == 0 && WN % 8 == 0, "warp tile");
+  constexpr uint32_t A_STAGE = BM * kBK * 8, B_STAGE = BN * kBK * 8;
+
+  extern __shared__ __align__(128) double smem[];
+  const uint32_t sA = smem_u32(smem);
+  const uint32_t sB = sA + STAGES * A_STAGE;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp % WARPS_M) * WM, wn0 = (warp / WARPS_M) * WN;
+  const i64 m0 = static_cast<i64>(blockIdx.x) * BM;
+  const i64 n0 = static_cast<i64>(blockIdx.y) * BN;
+  const i64 KT = ceil_div(p.K, kBK);
+
+  TileLoader<BM, BK, NT, VEC, TA> la;
+  TileLoader<BN, BK, NT, VEC, !TB> lb;
+  la.init(p.A, p.lda, m0, p.M, p.K);
+  lb.init(p.B, p.ldb, n0, p.N, p.K);
+
+  // Per-thread fragment offsets (bytes, within a stage) for k-step 0; later
+  // k-steps add a constant (the swizzle depends on row & 3 only, and k-steps
+  // move the k index by 4 rows in k-major layouts).
+  uint32_t a_off[TM][2], b_off[TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int m = wm0 + 16 * i + 8 * h + g;
+      a_off[i][h] = 8u * static_cast<uint32_t>(TA ? swz64(m, t, kBK) : swz64(t, m, BM));
+    }
+#pragma unroll
+  for (int j = 0; j < TN; ++j) {
+    const int n = wn0 + 8 * j + g;
+    b_off[j] = 8u * static_cast<uint32_t>(TB ? swz64(t, n, BN) : swz64(n, t, kBK));
+  }
+  // k-major layouts: a k-step moves 4 rows and keeps (row & 3), hence the
+  // swizzle; k-contiguous layouts recompute the swizzled column.
+  auto a_addr = [&](uint32_t stage, int i, int h, int kk) -> uint32_t {
+    if constexpr (!TA) return stage + a_off[i][h] + static_cast<uint32_t>(kk * 4 * BM * 8);
+    const int m = wm0 + 16 * i + 8 * h + g;
+    return stage + 8u * static_cast<uint32_t>(swz64(m, kk * 4 + t, kBK));
+  };
+  auto b_addr = [&](uint32_t stage, int j, int kk) -> uint32_t {
+    if constexpr (TB) return stage + b_off[j] + static_cast<uint32_t>(kk * 4 * BN * 8);
+    const int n = wn0 + 8 * j + g;
+    return stage + 8u * static_cast<uint32_t>(swz64(n, kk * 4 + t, kBK));
+  };
+
+  double af[2][TM][2], bf[2][TN];
+  auto load_frags = [&](int buf, int stage, int kk) {
+    const uint32_t as = sA + stage * A_STAGE, bs = sB + stage * B_STAGE;
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(af[buf][i][h]) : "r"(a_addr(as, i, h, kk)));
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+      asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(bf[buf][j]) : "r"(b_addr(bs, j, kk)));
+  };
+
+  double acc[TM][TN][4];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) {
+      la.load(sA + s * A_STAGE, s);
+      lb.load(sB + s * B_STAGE, s);
+    }
+    cp_async_commit();
+  }
+  cp_async_wait<STAGES - 2>();
+  __syncthreads();
+  load_frags(0, 0, 0);
+
+  for (i64 kt = 0; kt < KT; ++kt) {
+    {  // refill the stage of tile kt-1 (fully consumed before the last barrier)
+      const i64 nk = kt + STAGES - 1;
+      if (nk < KT) {
+        const int ws = static_cast<int>(nk % STAGES);
+        la.load(sA + ws * A_STAGE, nk);
+        lb.load(sB + ws * B_STAGE, nk);
+      }
+      cp_async_commit();
+    }
+    const int rs = static_cast<int>(kt % STAGES);
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk) {
+      const int cb = kk & 1, nb = cb ^ 1;
+      if (kk < KK - 1) {
+        load_frags(nb, rs, kk + 1);
+      } else {
+        cp_async_wait<STAGES - 2>();  // tile kt+1 has landed (this thread's part)
+        __syncthreads();              // ... and everyone's; stage rs-1 is free
+        if (kt + 1 < KT) load_frags(nb, static_cast<int>((kt + 1) % STAGES), 0);
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma1684(acc[i][j], af[cb][i][0], af[cb][i][1], bf[cb][j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  const bool beta_zero = p.beta == 0.0;
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const i64 m = m0 + wm0 + 16 * i + 8 * h + g;
+      if (m >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const i64 n = n0 + wn0 + 8 * j + 2 * t;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (n + e < p.N) {
+            double* c = p.C + m + (n + e) * p.ldc;
+            const double v = acc[i][j][2 * h + e];
+            *c = beta_zero ? p.alpha * v : fma(p.alpha, v, p.beta * *c);
+          }
+        }
+      }
+    }
+}
+
+// Host launcher of one configuration (all four transpose forms, both copy
+// widths); instantiated in gemm_f64_cfg*.cu.
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+struct Config {
+  template <bool TA, bool TB, int VEC>
+  static void launch(const GemmParams<double>& p, cudaStream_t s) {
+    auto kern = dgemm_dmma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TA, TB, VEC>;
+    constexpr int smem = STAGES * (BM + BN) * BK * static_cast<int>(sizeof(double));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
+    kern<<<grid, WARPS_M * WARPS_N * 32, smem, s>>>(p);
+    ++launch_counter();
+  }
+  static void run(const GemmParams<double>& p, bool ta, bool tb, bool vec2, cudaStream_t s) {
+#define RECTRI_T(TA_, TB_)                                  \
+  if (ta == TA_ && tb == TB_) {                             \
+    if (vec2) launch<TA_, TB_, 2>(p, s);                    \
+    else launch<TA_, TB_, 1>(p, s);                         \
+    return;                                                 \
+  }
+    RECTRI_T(false, false)
+    RECTRI_T(true, false)
+    RECTRI_T(false, true)
+    RECTRI_T(true, true)
+#undef RECTRI_T
+  }
+};
+
+}  // namespace dgemm
+
+// Entry points of the instantiated configurations (gemm_f64_cfg*.cu).
+using DgemmRun = void (*)(const GemmParams<double>&, bool, bool, bool, cudaStream_t);
+#define RECTRI_DGEMM_CONFIGS(X)          \
+  X(0, 128, 128, 16, 2, 4, 4)            \
+  X(1, 128, 128, 16, 4, 4, 4)            \
+  X(2, 128, 128, 32, 2, 4, 3)            \
+  X(3, 128, 128, 32, 4, 4, 3)            \
+  X(4, 128, 64, 16, 4, 2, 4)             \
+  X(5, 64, 128, 16, 2, 4, 4)             \
+  X(6, 64, 64, 16, 2, 2, 4)              \
+  X(7, 64, 128, 32, 2, 4, 3)             \
+  X(8, 128, 64, 32, 4, 2, 3)             \
+  X(9, 64, 64, 32, 2, 2, 3)              \
+  X(10, 64, 64, 16, 1, 2, 4)             \
+  X(11, 64, 64, 16, 2, 2, 3)             \
+  X(12, 64, 128, 16, 2, 2, 4)            \
+  X(13, 128, 64, 16, 2, 2, 4)            \
+  X(14, 64, 64, 16, 2, 1, 4)
+#define RECTRI_DECL(ID, BM, BN, BK, WM, WN, ST) \
+  void dgemm_cfg##ID(const GemmParams<double>&, bool, bool, bool, cudaStream_t);
+RECTRI_DGEMM_CONFIGS(RECTRI_DECL)
+#undef RECTRI_DECL
+
+}  // namespace rectri_cu

@@ -77,46 +77,62 @@ __device__ __forceinline__ const T* lprime_ptr(const LeafParams<T>& p, int r, in
   return p.A + row + col * p.lda;
 }
 
-// Off-diagonal block-row GEMM: acc(block I) += sign * Ls(32 x 32) * panel(block J).
-// fp64: warp w owns the m8n8 tiles (w & 3, 2*(w >> 2) + e), e = 0, 1.
+// Off-diagonal block-row GEMM: acc(block I) += Ls(32 x 32) * panel(block J).
+// TRSM accumulates the NEGATED right-hand side (acc = -b + sum L'x) and
+// negates on store: with round-to-nearest every intermediate is the exact
+// negation of the b - sum L'x chain, so no per-element sign is needed.
+// fp64: warp w owns the m8n8 tiles (w & 3, 2*(w >> 2) + e), e = 0, 1;
+// fragment addresses are fixed per thread (row & 3 is invariant).
 struct GemmPart64 {
   double c[2][2];
   int mt, nt0, g, t;
+  uint32_t a_base, b_base[2];  // shared byte offsets for k-step 0
   __device__ void init(int lane, int warp) {
     g = lane >> 2;
     t = lane & 3;
     mt = warp & 3;
     nt0 = 2 * (warp >> 2);
+    a_base = 8u * static_cast<uint32_t>(swz64(t, 8 * mt + g, kRB));
+#pragma unroll
+    for (int e = 0; e < 2; ++e) b_base[e] = 8u * static_cast<uint32_t>(swz64(t, 8 * (nt0 + e) + g, kNC));
   }
-  __device__ void load(const double* panel, int r0) {
+  __device__ void load(const double* panel, int r0, bool negate) {
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        c[e][h] = panel[Layout<double>::panel(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)];
+      for (int h = 0; h < 2; ++h) {
+        const double x = panel[Layout<double>::panel(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)];
+        c[e][h] = negate ? -x : x;
+      }
   }
   __device__ void zero() {
 #pragma unroll
     for (int e = 0; e < 2; ++e) c[e][0] = c[e][1] = 0.0;
   }
-  __device__ void mma(const double* ls, const double* panel, int j0, double sign) {
+  // ls_u32 / panel_u32: shared addresses of the staged block and the panel.
+  __device__ void mma(uint32_t ls_u32, uint32_t panel_u32, int j0) {
+    double a[2], b[2][2];
+    const uint32_t pb = panel_u32 + static_cast<uint32_t>(j0 * kNC * 8);
+    auto ld = [&](int buf, int kk) {
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[buf]) : "r"(ls_u32 + a_base + kk * 4 * kRB * 8));
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b[buf][e]) : "r"(pb + b_base[e] + kk * 4 * kNC * 8));
+    };
+    ld(0, 0);
 #pragma unroll
     for (int kk = 0; kk < kRB / 4; ++kk) {
-      const int k = 4 * kk + t;
-      const double a = ls[swz64(k, 8 * mt + g, kRB)];
+      if (kk + 1 < kRB / 4) ld((kk + 1) & 1, kk + 1);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const double b = sign * panel[Layout<double>::panel(j0 + k, 8 * (nt0 + e) + g)];
-        dmma884(c[e][0], c[e][1], a, b);
-      }
+      for (int e = 0; e < 2; ++e) dmma884(c[e][0], c[e][1], a[kk & 1], b[kk & 1][e]);
     }
   }
-  __device__ void store(double* dst, int r0) const {
+  __device__ void store(double* dst, int r0, bool negate) const {
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
       for (int h = 0; h < 2; ++h)
-        dst[Layout<double>::panel(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
+        dst[Layout<double>::panel(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = negate ? -c[e][h] : c[e][h];
   }
 };
 
@@ -128,18 +144,23 @@ struct GemmPart32 {
     lane = lane_;
     w = warp;
   }
-  __device__ void load(const float* panel, int r0) {
+  __device__ void load(const float* panel, int r0, bool negate) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) c[i] = panel[Layout<float>::panel(r0 + 4 * w + i, lane)];
+    for (int i = 0; i < 4; ++i) {
+      const float x = panel[Layout<float>::panel(r0 + 4 * w + i, lane)];
+      c[i] = negate ? -x : x;
+    }
   }
   __device__ void zero() {
 #pragma unroll
     for (int i = 0; i < 4; ++i) c[i] = 0.f;
   }
-  __device__ void mma(const float* ls, const float* panel, int j0, float sign) {
+  __device__ void mma(uint32_t ls_u32, uint32_t panel_u32, int j0) {
+    const float* ls = reinterpret_cast<const float*>(__cvta_shared_to_generic(ls_u32));
+    const float* panel = reinterpret_cast<const float*>(__cvta_shared_to_generic(panel_u32));
 #pragma unroll 8
     for (int k = 0; k < kRB; ++k) {
-      const float b = sign * panel[Layout<float>::panel(j0 + k, lane)];
+      const float b = panel[Layout<float>::panel(j0 + k, lane)];
       const float4 a = *reinterpret_cast<const float4*>(ls + k * kRB + 4 * w);
       c[0] = fmaf(a.x, b, c[0]);
       c[1] = fmaf(a.y, b, c[1]);
@@ -147,9 +168,9 @@ struct GemmPart32 {
       c[3] = fmaf(a.w, b, c[3]);
     }
   }
-  __device__ void store(float* dst, int r0) const {
+  __device__ void store(float* dst, int r0, bool negate) const {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) dst[Layout<float>::panel(r0 + 4 * w + i, lane)] = c[i];
+    for (int i = 0; i < 4; ++i) dst[Layout<float>::panel(r0 + 4 * w + i, lane)] = negate ? -c[i] : c[i];
   }
 };
 
@@ -164,23 +185,45 @@ struct GemmPartOf<float> {
   using type = GemmPart32;
 };
 
+constexpr int kRing = 4;  // depth of the staged-block ring
+
 template <typename T>
 struct LeafSmem {
   static constexpr int panel = kLeafMax * Layout<T>::kPanelStride;
   static constexpr int blk = kRB * kRB;
   static constexpr int ys = kRB * Layout<T>::kPanelStride;
-  static constexpr int total = panel + 3 * blk + ys + kLeafMax;
+  static constexpr int total = panel + kRing * blk + ys + kLeafMax;
 };
+
+// The blocks of L' a CTA consumes, in order: for each row block I (ascending
+// for TRSM, descending for TRMM) its off-diagonal blocks J = 0 .. I-1, then
+// its diagonal block.  Element s of that sequence -> (I, J), J == I meaning
+// the diagonal block.
+__device__ __forceinline__ void seq_block(int s, int nblk, bool ascending, int& I, int& J) {
+  // Row block order index q has q+1 elements (q off-diagonal + 1 diagonal)
+  // when ascending (I = q), or I+1 elements with I = nblk-1-q otherwise.
+  int q = 0, base = 0;
+  while (true) {
+    const int Iq = ascending ? q : nblk - 1 - q;
+    const int len = Iq + 1;
+    if (s < base + len) {
+      I = Iq;
+      J = s - base;
+      return;
+    }
+    base += len;
+    ++q;
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
   using L = Layout<T>;
   extern __shared__ __align__(128) unsigned char leaf_smem[];
   T* panel = reinterpret_cast<T*>(leaf_smem);
-  T* ls = panel + LeafSmem<T>::panel;  // two staged off-diagonal blocks of L'
-  T* ld = ls + 2 * LeafSmem<T>::blk;   // diagonal block, ld[p * 32 + r] = L'(r, p), p < r
-  T* ys = ld + LeafSmem<T>::blk;       // TRMM off-diagonal partial sums
-  T* dg = ys + LeafSmem<T>::ys;        // TRSM: 1 / d_r; TRMM: d_r (1 for Unit)
+  T* ring = panel + LeafSmem<T>::panel;          // kRing staged 32x32 blocks of L'
+  T* ys = ring + kRing * LeafSmem<T>::blk;       // TRMM off-diagonal partial sums
+  T* dg = ys + LeafSmem<T>::ys;                  // TRSM: 1 / d_r; TRMM: d_r (1 for Unit)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = p.n;
@@ -188,6 +231,7 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
   const int rows_p = nblk * kRB;
   const i64 c0 = static_cast<i64>(blockIdx.x) * kNC;
   const int ncols = static_cast<int>(min(static_cast<i64>(kNC), p.nrhs - c0));
+  const bool asc = p.trsm != 0;  // TRMM runs bottom-up (in place)
 
   auto gaddr = [&](int r, int c) -> i64 {  // global offset of B'(r, c0 + c)
     const i64 sr = p.reflected ? n - 1 - r : r;
@@ -217,33 +261,23 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
     return;
   }
 
-  // 1. Panel load.
-  for (int q = tid; q < rows_p * kNC; q += kThreads) {
-    int r, c;
-    panel_rc(q, r, c);
-    const bool ok = r < n && c < ncols;
-    cp_async_elem(panel + L::panel(r, c), ok ? p.B + gaddr(r, c) : p.B, ok);
-  }
-  cp_async_commit();
-  for (int r = tid; r < rows_p; r += kThreads) {
-    T d = T(1);
-    if (r < n && !p.unit) {
-      const i64 sr = p.reflected ? n - 1 - r : r;
-      d = p.A[sr + sr * p.lda];
-    }
-    dg[r] = p.trsm ? T(1) / d : d;
-  }
-
-  // Staging of a 32x32 block of L' (rows r0.., k-columns j0..) with
-  // masking: entries with j >= r (diagonal block) or outside n are zero.
-  // Each warp copies 4 k-columns x 8 rows per step.
-  auto stage_block = [&](T* dst, int r0, int j0, bool diag) {
+  // Staging of sequence element s into its ring slot.  Off-diagonal blocks
+  // are stored k-major for the GEMM part (each warp copies 4 k x 8 rows);
+  // the diagonal block as [p][r] = L'(r, p) for p < r, zero elsewhere.
+  // Masked / out-of-range entries are zero-filled (never read).
+  const int nseq = nblk * (nblk + 1) / 2;
+  auto stage = [&](int s) {
+    int I, J;
+    seq_block(s, nblk, asc, I, J);
+    T* dst = ring + (s % kRing) * LeafSmem<T>::blk;
+    const bool diag = I == J;
+    const int r0 = I * kRB, j0 = J * kRB;
 #pragma unroll
     for (int it = 0; it < kRB * kRB / kThreads; ++it) {
       const int q = tid + it * kThreads;
       const int w = q >> 5, l = q & 31;
       int r, j;
-      if (diag) {  // row pattern (conflict-free for the [p][r] layout)
+      if (diag) {
         r = l;
         j = w;
       } else {
@@ -252,12 +286,33 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
       }
       const int gr = r0 + r, gj = j0 + j;
       const bool ok = gr < n && (diag ? j < r : true);
-      T* s = diag ? dst + j * kRB + r : dst + L::lblk(r, j);
-      cp_async_elem(s, ok ? lprime_ptr(p, gr, gj) : p.A, ok);
+      T* sdst = diag ? dst + j * kRB + r : dst + L::lblk(r, j);
+      cp_async_elem(sdst, ok ? lprime_ptr(p, gr, gj) : p.A, ok);
     }
   };
 
-  cp_async_wait<0>();
+  // 1. Panel load + the first ring elements (one commit group each).
+  for (int q = tid; q < rows_p * kNC; q += kThreads) {
+    int r, c;
+    panel_rc(q, r, c);
+    const bool ok = r < n && c < ncols;
+    cp_async_elem(panel + L::panel(r, c), ok ? p.B + gaddr(r, c) : p.B, ok);
+  }
+  cp_async_commit();
+#pragma unroll
+  for (int s = 0; s < kRing - 1; ++s) {
+    if (s < nseq) stage(s);
+    cp_async_commit();
+  }
+  for (int r = tid; r < rows_p; r += kThreads) {
+    T d = T(1);
+    if (r < n && !p.unit) {
+      const i64 sr = p.reflected ? n - 1 - r : r;
+      d = p.A[sr + sr * p.lda];
+    }
+    dg[r] = p.trsm ? T(1) / d : d;
+  }
+  cp_async_wait<kRing - 1>();  // the panel group
   __syncthreads();
   if (p.trsm && p.alpha != T(1)) {  // x = alpha * b (base_kernels.cpp:76-77)
     for (int q = tid; q < rows_p * kNC; q += kThreads) {
@@ -265,49 +320,40 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
       panel_rc(q, r, c);
       panel[L::panel(r, c)] *= p.alpha;
     }
-    __syncthreads();
   }
 
   typename GemmPartOf<T>::type gp;
   gp.init(lane, warp);
-  const T sign = p.trsm ? T(-1) : T(1);
+  const uint32_t panel_u32 = smem_u32(panel);
+  const uint32_t ring_u32 = smem_u32(ring);
   // Diagonal-part thread roles: column cc, row group gq (rows gq + 8q).
   const int cc = warp * 4 + (lane >> 3);
   const int gq = lane & 7;
+  const bool neg = p.trsm != 0;
 
-  for (int step = 0; step < nblk; ++step) {
-    const int I = p.trsm ? step : nblk - 1 - step;  // TRMM runs bottom-up (in place)
-    const int r0 = I * kRB;
-
-    // Prefetch: the diagonal block, then the first off-diagonal block.
-    stage_block(ld, r0, r0, true);
+  for (int s = 0; s < nseq; ++s) {
+    cp_async_wait<kRing - 2>();  // element s has landed (this thread's copies)
+    __syncthreads();              // ... everyone's; slot (s-1) % kRing is free
+    if (s + kRing - 1 < nseq) stage(s + kRing - 1);
     cp_async_commit();
-    if (I > 0) {
-      stage_block(ls, r0, 0, false);
-      cp_async_commit();
-    }
 
-    // 2. Off-diagonal block-row GEMM, block J+1 in flight while J multiplies.
-    if (p.trsm) gp.load(panel, r0);
-    else gp.zero();
-    for (int J = 0; J < I; ++J) {
-      if (J + 1 < I) {
-        stage_block(ls + ((J + 1) & 1) * LeafSmem<T>::blk, r0, (J + 1) * kRB, false);
-        cp_async_commit();
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncthreads();
-      gp.mma(ls + (J & 1) * LeafSmem<T>::blk, panel, J * kRB, sign);
-      __syncthreads();
+    int I, J;
+    seq_block(s, nblk, asc, I, J);
+    const int r0 = I * kRB;
+    const uint32_t slot = ring_u32 + static_cast<uint32_t>((s % kRing) * LeafSmem<T>::blk * sizeof(T));
+    if (J == 0) {  // first element of row block I: fresh accumulators
+      if (p.trsm) gp.load(panel, r0, neg);
+      else gp.zero();
     }
-    if (p.trsm) gp.store(panel, r0);
-    else gp.store(ys, 0);
-    cp_async_wait<0>();
+    if (J < I) {  // 2. off-diagonal block-row GEMM
+      gp.mma(slot, panel_u32, J * kRB);
+      continue;
+    }
+    // 3. diagonal block (slot holds ld[p * 32 + r] = L'(r, p), p < r).
+    const T* ld = ring + (s % kRing) * LeafSmem<T>::blk;
+    if (p.trsm) gp.store(panel, r0, neg);
+    else gp.store(ys, 0, false);
     __syncthreads();
-
-    // 3. Diagonal block.
     T v[4];
     if (p.trsm) {
 #pragma unroll
@@ -346,8 +392,9 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) panel[L::panel(r0 + gq + 8 * q, cc)] = p.alpha * v[q];
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
+  __syncthreads();
 
   // 4. Write back.
   for (int q = tid; q < rows_p * kNC; q += kThreads) {
