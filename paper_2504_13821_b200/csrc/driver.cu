@@ -281,8 +281,8 @@ template <typename T>
 class Recursion {
  public:
   Recursion(OpK op, i64 threshold, cudaStream_t s, std::vector<Ev>* events,
-            std::vector<std::pair<i64, i64>>* leaves)
-      : op_(op), threshold_(threshold), s_(s), events_(events), leaves_(leaves) {}
+            std::vector<std::pair<i64, i64>>* leaves, bool dry = false)
+      : op_(op), threshold_(threshold), s_(s), events_(events), leaves_(leaves), dry_(dry) {}
 
   // recursion.cpp:85-148
   void run(const Spec& spec, DView<const T> A, DView<T> B, i64 row0) {
@@ -291,7 +291,7 @@ class Recursion {
     if (n <= threshold_) {
       emit(op_ == kTrmm ? RECTRI_CU_EV_BASE_TRMM : RECTRI_CU_EV_BASE_TRSM, n, rhs);
       if (leaves_) leaves_->push_back({row0, n});
-      enqueue_base<T>(op_, spec, A, B, s_);
+      if (!dry_) enqueue_base<T>(op_, spec, A, B, s_);
       return;
     }
     const i64 mid = n / 2;  // split_half
@@ -311,7 +311,8 @@ class Recursion {
     const DView<const T> src = sc.read_b2 ? b2 : b1;
     const T coeff = static_cast<T>(sc.sign * (sc.carries_alpha ? spec.alpha : 1.0));
     emit(RECTRI_CU_EV_GEMM, dst.rows, dst.cols);
-    if (sc.off_on_left)
+    if (dry_) {
+    } else if (sc.off_on_left)
       enqueue_gemm<T>(coeff, sc.off_trans != 0, off, false, src, T(1), dst, s_);
     else
       enqueue_gemm<T>(coeff, false, src, sc.off_trans != 0, off, T(1), dst, s_);
@@ -329,6 +330,7 @@ class Recursion {
   cudaStream_t s_;
   std::vector<Ev>* events_;
   std::vector<std::pair<i64, i64>>* leaves_;
+  bool dry_;
 };
 
 template <typename T>
@@ -364,8 +366,10 @@ void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaSt
 // Per-device resources: capture stream and a staging pool for host views.
 struct DeviceRes {
   cudaStream_t capture = nullptr;
-  void* stage[2] = {nullptr, nullptr};
-  size_t stage_bytes[2] = {0, 0};
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the staged path
+  static constexpr int kSlots = 3;            // 0: A, 1..2: B panels
+  void* stage[kSlots] = {nullptr, nullptr, nullptr};
+  size_t stage_bytes[kSlots] = {0, 0, 0};
 };
 
 std::mutex g_mu;
@@ -373,7 +377,11 @@ std::map<int, DeviceRes> g_dev;
 
 DeviceRes& device_res(int dev) {
   DeviceRes& r = g_dev[dev];
-  if (!r.capture) cuda_check(cudaStreamCreateWithFlags(&r.capture, cudaStreamNonBlocking), "stream");
+  if (!r.capture) {
+    cuda_check(cudaStreamCreateWithFlags(&r.capture, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&r.h2d, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking), "stream");
+  }
   return r;
 }
 
@@ -516,52 +524,167 @@ uint64_t bits_of(double a) {
   return b;
 }
 
-// Device-resident recursive call (both views on the device of `dev`).
+// Enqueues one device-resident recursive call (both views on the device of
+// `dev`) on `stream`: from the graph cache (captured on first use) or by
+// direct launches.  Replays the call's events to `sink` when given.
+template <typename T>
+std::shared_ptr<GraphEntry> enqueue_device(OpK op, const Spec& spec, DView<const T> A, DView<T> B,
+                                           i64 threshold, cudaStream_t stream, unsigned flags,
+                                           rectri_cu_event_fn sink, void* user, int dev) {
+  std::shared_ptr<GraphEntry> g;
+  if ((flags & RECTRI_CU_NO_GRAPH) || g_prof.on) {
+    g = build<T>(op, spec, A, B, threshold, stream, false, dev);
+    for (const Ev& e : g->events)
+      if (sink) sink(user, e.e, e.n, e.m);
+    return g;
+  }
+  const Key key{static_cast<int>(op), dtype_code<T>(), spec.side, spec.uplo, spec.trans,
+                spec.diag, bits_of(spec.alpha), static_cast<const void*>(A.p), A.ld, A.rows,
+                static_cast<void*>(B.p), B.ld, B.rows, B.cols, threshold, dev};
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    g = g_cache.get(key);
+    if (!g) {
+      DeviceRes& res = device_res(dev);
+      g = build<T>(op, spec, A, B, threshold, res.capture, true, dev);
+      g_cache.put(key, g);
+    }
+  }
+  for (const Ev& e : g->events)
+    if (sink) sink(user, e.e, e.n, e.m);
+  cuda_check(cudaGraphLaunch(g->exec, stream), "graph launch");
+  launch_counter() += g->nodes;
+  return g;
+}
+
+void raise_if_singular(const GraphEntry& g) {
+  if (!g.h_flags) return;
+  const i64 r = first_singular(g);
+  if (r >= 0) {
+    Fail f{RECTRI_CU_SINGULAR, "singular triangular matrix: zero diagonal at row " + std::to_string(r)};
+    f.index = r;
+    throw f;
+  }
+}
+
+// Device-resident recursive call: enqueue, then synchronize and report
+// singularity (or defer both under RECTRI_CU_ASYNC).
 template <typename T>
 void run_device(OpK op, const Spec& spec, DView<const T> A, DView<T> B, i64 threshold,
                 const BackendInfo& be, rectri_cu_event_fn sink, void* user, int dev,
                 bool force_sync) {
-  cudaStream_t user_s = be.stream;
   const bool async = (be.flags & RECTRI_CU_ASYNC) && !force_sync;
-  std::shared_ptr<GraphEntry> g;
-  if ((be.flags & RECTRI_CU_NO_GRAPH) || g_prof.on) {
-    g = build<T>(op, spec, A, B, threshold, user_s, false, dev);
-    for (const Ev& e : g->events)
-      if (sink) sink(user, e.e, e.n, e.m);
-  } else {
-    const Key key{static_cast<int>(op), dtype_code<T>(), spec.side, spec.uplo, spec.trans,
-                  spec.diag, bits_of(spec.alpha), static_cast<const void*>(A.p), A.ld, A.rows,
-                  static_cast<void*>(B.p), B.ld, B.rows, B.cols, threshold, dev};
-    {
-      std::lock_guard<std::mutex> lock(g_mu);
-      g = g_cache.get(key);
-      if (!g) {
-        DeviceRes& res = device_res(dev);
-        g = build<T>(op, spec, A, B, threshold, res.capture, true, dev);
-        g_cache.put(key, g);
-      }
-    }
-    for (const Ev& e : g->events)
-      if (sink) sink(user, e.e, e.n, e.m);
-    cuda_check(cudaGraphLaunch(g->exec, user_s), "graph launch");
-    launch_counter() += g->nodes;
-  }
+  std::shared_ptr<GraphEntry> g =
+      enqueue_device<T>(op, spec, A, B, threshold, be.stream, be.flags, sink, user, dev);
   if (async) {
     if (g->h_flags) {
       std::lock_guard<std::mutex> lock(g_mu);
-      g_pending.emplace(user_s, g);
+      g_pending.emplace(be.stream, g);
     }
     return;
   }
-  cuda_check(cudaStreamSynchronize(user_s), "synchronize");
-  if (g->h_flags) {
-    const i64 r = first_singular(*g);
-    if (r >= 0) {
-      Fail f{RECTRI_CU_SINGULAR, "singular triangular matrix: zero diagonal at row " + std::to_string(r)};
-      f.index = r;
-      throw f;
-    }
+  cuda_check(cudaStreamSynchronize(be.stream), "synchronize");
+  raise_if_singular(*g);
+}
+
+// Copies the stored triangle of a host n x n A (the only part the kernels
+// ever read: uplo triangle incl. diagonal) into a dense device n x n buffer,
+// as column-block trapezoids.
+template <typename T>
+void copy_triangle_h2d(T* dA, const DView<const T>& A, int uplo, cudaStream_t s) {
+  const i64 n = A.rows;
+  constexpr i64 kW = 512;
+  for (i64 c0 = 0; c0 < n; c0 += kW) {
+    const i64 w = c0 + kW < n ? kW : n - c0;
+    const i64 r0 = uplo == RECTRI_CU_LOWER ? c0 : 0;
+    const i64 r1 = uplo == RECTRI_CU_LOWER ? n : c0 + w;
+    cuda_check(cudaMemcpy2DAsync(dA + c0 * n + r0, sizeof(T) * n, A.p + c0 * A.ld + r0, sizeof(T) * A.ld,
+                                 sizeof(T) * (r1 - r0), w, cudaMemcpyHostToDevice, s),
+               "H2D A");
   }
+}
+
+// Host-resident B: the right-hand sides are cut into panels; H2D of panel
+// i+1, the recursion on panel i and D2H of panel i-1 run concurrently on
+// three streams (two device panel slots).  Kernels are independent of the
+// number of right-hand sides, so the result is bitwise the unpanelled one;
+// the event sink sees the single logical call.
+template <typename T>
+void run_host_panels(OpK op, const Spec& spec, DView<const T> dA, DView<T> hB, i64 threshold,
+                     const BackendInfo& be, rectri_cu_event_fn sink, void* user, int dev,
+                     cudaEvent_t a_ready) {
+  const bool left = spec.side == RECTRI_CU_LEFT;
+  const i64 n = dA.rows;
+  const i64 rhs = left ? hB.cols : hB.rows;
+  // Panel width: a few panels for overlap, none narrower than 2048.
+  i64 w = (rhs + 3) / 4;
+  if (w < 2048) w = 2048;
+  if (w > rhs) w = rhs;
+  const i64 np = (rhs + w - 1) / w;
+
+  // Events of the single logical call (recursion.cpp:94, 97, 139).
+  if (sink) {
+    std::vector<Ev> evs;
+    Spec eff = spec;
+    Recursion<T>(op, threshold, nullptr, &evs, nullptr, true)
+        .run(eff, dA, DView<T>{nullptr, hB.ld, hB.rows, hB.cols}, 0);
+    for (const Ev& e : evs) sink(user, e.e, e.n, e.m);
+  }
+
+  DeviceRes* res;
+  T* slot[2];
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    res = &device_res(dev);
+    for (int k = 0; k < 2; ++k)
+      slot[k] = static_cast<T*>(staging(*res, 1 + k, static_cast<size_t>(n * w) * sizeof(T)));
+  }
+  cudaStream_t cs = be.stream, hs = res->h2d, ds = res->d2h;
+  std::vector<cudaEvent_t> evs;
+  auto ev = [&]() {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    evs.push_back(e);
+    return e;
+  };
+  cudaEvent_t slot_free[2] = {nullptr, nullptr};
+  std::shared_ptr<GraphEntry> first;
+  try {
+    if (a_ready) cuda_check(cudaStreamWaitEvent(hs, a_ready, 0), "wait A");
+    for (i64 i = 0; i < np; ++i) {
+      const i64 r0 = i * w, wi = r0 + w <= rhs ? w : rhs - r0;
+      const int k = static_cast<int>(i & 1);
+      // panel i in the slot's own packed layout (Left: n x wi, Right: wi x n)
+      const DView<T> d = left ? DView<T>{slot[k], n, n, wi} : DView<T>{slot[k], wi, wi, n};
+      const T* hsrc = left ? hB.p + r0 * hB.ld : hB.p + r0;
+      if (slot_free[k]) cuda_check(cudaStreamWaitEvent(hs, slot_free[k], 0), "wait slot");
+      cuda_check(cudaMemcpy2DAsync(d.p, sizeof(T) * d.ld, hsrc, sizeof(T) * hB.ld, sizeof(T) * d.rows,
+                                   d.cols, cudaMemcpyHostToDevice, hs),
+                 "H2D B panel");
+      cudaEvent_t in = ev();
+      cuda_check(cudaEventRecord(in, hs), "record");
+      cuda_check(cudaStreamWaitEvent(cs, in, 0), "wait panel");
+      auto g = enqueue_device<T>(op, spec, dA, d, threshold, cs, be.flags, nullptr, nullptr, dev);
+      if (!first) first = g;
+      cudaEvent_t done = ev();
+      cuda_check(cudaEventRecord(done, cs), "record");
+      cuda_check(cudaStreamWaitEvent(ds, done, 0), "wait compute");
+      cuda_check(cudaMemcpy2DAsync(const_cast<T*>(hsrc), sizeof(T) * hB.ld, d.p, sizeof(T) * d.ld,
+                                   sizeof(T) * d.rows, d.cols, cudaMemcpyDeviceToHost, ds),
+                 "D2H B panel");
+      slot_free[k] = ev();
+      cuda_check(cudaEventRecord(slot_free[k], ds), "record");
+    }
+    cuda_check(cudaStreamSynchronize(ds), "synchronize");
+    cuda_check(cudaStreamSynchronize(cs), "synchronize");
+  } catch (...) {
+    cudaStreamSynchronize(ds);
+    cudaStreamSynchronize(cs);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    throw;
+  }
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  if (first) raise_if_singular(*first);
 }
 
 // rec_trmm / rec_trsm entry (recursion.cpp:165-192).
@@ -597,48 +720,31 @@ void rec_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
                   dev, false);
     return;
   }
-  // Host-resident operands: stage to the device, compute, copy B back.
+  // Host-resident operands: A's stored triangle is staged once; a host B is
+  // processed in pipelined panels (run_host_panels).
   const i64 n = Av.rows;
   cudaStream_t s = be.stream;
   DView<const T> A = dview_of<const T>(Av);
   DView<T> B = dview_of<T>(Bv);
   DView<const T> dA = A;
-  DView<T> dB = B;
+  DeviceRes* res;
   {
     std::lock_guard<std::mutex> lock(g_mu);
-    DeviceRes& res = device_res(dev);
-    if (!a_dev) {
-      T* p = static_cast<T*>(staging(res, 0, static_cast<size_t>(n * n) * sizeof(T)));
-      dA = DView<const T>{p, n, n, n};
-    }
-    if (!b_dev) {
-      T* p = static_cast<T*>(staging(res, 1, static_cast<size_t>(B.rows * B.cols) * sizeof(T)));
-      dB = DView<T>{p, B.rows, B.rows, B.cols};
-    }
+    res = &device_res(dev);
+    if (!a_dev) dA = DView<const T>{static_cast<T*>(staging(*res, 0, static_cast<size_t>(n * n) * sizeof(T))), n, n, n};
   }
-  if (!a_dev)
-    cuda_check(cudaMemcpy2DAsync(const_cast<T*>(dA.p), sizeof(T) * n, A.p, sizeof(T) * A.ld,
-                                 sizeof(T) * n, n, cudaMemcpyHostToDevice, s),
-               "H2D A");
-  if (!b_dev)
-    cuda_check(cudaMemcpy2DAsync(dB.p, sizeof(T) * dB.ld, B.p, sizeof(T) * B.ld,
-                                 sizeof(T) * B.rows, B.cols, cudaMemcpyHostToDevice, s),
-               "H2D B");
   BackendInfo be2 = be;
   be2.flags &= ~RECTRI_CU_ASYNC;
-  try {
-    run_device<T>(op, spec, dA, dB, threshold, be2, sink, user, dev, true);
-  } catch (const Fail& f) {
-    if (f.code != RECTRI_CU_SINGULAR) throw;
-    // B is unspecified after a singularity error; leave the host copy as is.
-    throw;
+  if (b_dev) {
+    if (!a_dev) copy_triangle_h2d<T>(const_cast<T*>(dA.p), A, spec.uplo, s);
+    run_device<T>(op, spec, dA, B, threshold, be2, sink, user, dev, true);
+    return;
   }
-  if (!b_dev) {
-    cuda_check(cudaMemcpy2DAsync(B.p, sizeof(T) * B.ld, dB.p, sizeof(T) * dB.ld,
-                                 sizeof(T) * B.rows, B.cols, cudaMemcpyDeviceToHost, s),
-               "D2H B");
-    cuda_check(cudaStreamSynchronize(s), "synchronize");
+  cudaEvent_t a_ready = nullptr;
+  if (!a_dev) {
+    copy_triangle_h2d<T>(const_cast<T*>(dA.p), A, spec.uplo, res->h2d);
   }
+  run_host_panels<T>(op, spec, dA, B, threshold, be2, sink, user, dev, a_ready);
 }
 
 // Temporary device copies of host views for the non-recursive entry points.

@@ -18,52 +18,65 @@ namespace {
 constexpr int kBK = 16;
 constexpr int kPad = 4;  // floats of row padding (keeps 16-byte alignment)
 
-// Shared layout for both operands: [k][o] with row stride BO + kPad.
-// Outer-contiguous source: element (o, k) at X[o + k * ld].
-template <int BO, int NT, int VEC>
-__device__ __forceinline__ void load_mc(float* s, const float* X, i64 ld, i64 o0, i64 O, i64 k0,
-                                        i64 K) {
-  constexpr int RS = BO + kPad;
-  if constexpr (VEC == 4) {
-    constexpr int CPR = BO / 4;
-#pragma unroll
-    for (int q = threadIdx.x; q < kBK * CPR; q += NT) {
-      const int k = q / CPR, oc = q % CPR;
-      const i64 go = o0 + 4 * oc, gk = k0 + k;
-      int bytes = 0;
-      const float* src = X;
-      if (gk < K && go < O) {
-        const i64 rem = O - go;
-        bytes = rem >= 4 ? 16 : static_cast<int>(rem) * 4;
-        src = X + go + gk * ld;
-      }
-      cp_async16(s + k * RS + 4 * oc, src, bytes);
-    }
-  } else {
-#pragma unroll 4
-    for (int q = threadIdx.x; q < kBK * BO; q += NT) {
-      const int k = q / BO, o = q % BO;
-      const i64 go = o0 + o, gk = k0 + k;
-      const bool ok = gk < K && go < O;
-      cp_async4(s + k * RS + o, ok ? X + go + gk * ld : X, ok ? 4 : 0);
-    }
-  }
-}
+// Per-thread loader of one operand tile.  Shared layout for both operands:
+// [k][o] rows of BO + kPad floats.
+//   MC (outer-contiguous source, element (o, k) at X[o + k*ld]): VEC-float
+//     chunks along o; the thread's o is fixed, its k advances by NT / CPR.
+//   KC (k-contiguous source, element (o, k) at X[k + o*ld]): transposed by
+//     4-byte copies, consecutive threads walk k (contiguous global
+//     addresses); the thread's k is fixed, its o advances by NT / kBK.
+// The thread's global pointer is computed once and advanced per k-tile.
+template <int BO, int NT, int VEC, bool KC>
+struct FLoader {
+  static constexpr int RS = BO + kPad;
+  static constexpr int CPR = KC ? kBK : BO / VEC;  // copies per shared row (KC: per o)
+  static constexpr int IT = kBK * BO / VEC / NT;
+  static constexpr int STEP = NT / CPR;            // MC: k rows, KC: o rows per iteration
+  static_assert(!KC || VEC == 1, "KC copies are 4-byte transposes");
+  static_assert(NT % CPR == 0 && (kBK * BO / VEC) % NT == 0, "loader trip count");
 
-// k-contiguous source: element (o, k) at X[k + o * ld]; transposed by 4-byte
-// copies (consecutive threads walk k, i.e. contiguous global addresses).
-template <int BO, int NT>
-__device__ __forceinline__ void load_kc(float* s, const float* X, i64 ld, i64 o0, i64 O, i64 k0,
-                                        i64 K) {
-  constexpr int RS = BO + kPad;
-#pragma unroll 4
-  for (int q = threadIdx.x; q < kBK * BO; q += NT) {
-    const int k = q & (kBK - 1), o = q / kBK;
-    const i64 go = o0 + o, gk = k0 + k;
-    const bool ok = gk < K && go < O;
-    cp_async4(s + k * RS + o, ok ? X + gk + go * ld : X, ok ? 4 : 0);
+  const float* base;
+  const float* p0;
+  i64 ld, step;
+  int k_first, o_first;
+  int o_lim, k_lim, fix_bytes;
+
+  __device__ void init(const float* X, i64 ld_, i64 o0, i64 O, i64 K) {
+    ld = ld_;
+    const int q = threadIdx.x;
+    if (KC) {
+      k_first = q % kBK;
+      o_first = q / kBK;
+    } else {
+      o_first = (q % CPR) * VEC;
+      k_first = q / CPR;
+    }
+    o_lim = static_cast<int>(O - o0 < (1 << 30) ? O - o0 : (1 << 30));
+    k_lim = static_cast<int>(K < (1 << 30) ? K : (1 << 30));
+    base = KC ? X + o0 * ld : X + o0;
+    p0 = KC ? base + static_cast<i64>(o_first) * ld + k_first : base + o_first + static_cast<i64>(k_first) * ld;
+    step = static_cast<i64>(STEP) * ld;
+    const int rem = o_lim - o_first;
+    fix_bytes = rem >= VEC ? VEC * 4 : (rem > 0 ? rem * 4 : 0);
   }
-}
+
+  __device__ __forceinline__ void load(float* s, i64 kt) const {
+    const int k0 = static_cast<int>(kt * kBK);
+    const float* tb = p0 + (KC ? static_cast<i64>(k0) : static_cast<i64>(k0) * ld);
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int o = o_first + (KC ? it * STEP : 0);
+      const int k = k_first + (KC ? 0 : it * STEP);
+      int bytes;
+      if (KC) bytes = (o < o_lim && k0 + k < k_lim) ? 4 : 0;
+      else bytes = (k0 + k < k_lim) ? fix_bytes : 0;
+      const float* g = bytes ? tb + it * step : base;
+      float* dst = s + k * RS + o;
+      if constexpr (VEC == 4) cp_async16(dst, g, bytes);
+      else cp_async4(dst, g, bytes);
+    }
+  }
+};
 
 template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB>
 __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
@@ -79,14 +92,13 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
   const i64 n0 = static_cast<i64>(blockIdx.y) * BN;
   const i64 KT = ceil_div(p.K, kBK);
 
+  FLoader<BM, NT, TA ? 1 : VA, TA> la;
+  FLoader<BN, NT, TB ? VB : 1, !TB> lb;
+  la.init(p.A, p.lda, m0, p.M, p.K);
+  lb.init(p.B, p.ldb, n0, p.N, p.K);
   auto load_stage = [&](int stage, i64 kt) {
-    const i64 k0 = kt * kBK;
-    float* a = sA + stage * kBK * RSA;
-    float* b = sB + stage * kBK * RSB;
-    if constexpr (TA) load_kc<BM, NT>(a, p.A, p.lda, m0, p.M, k0, p.K);
-    else load_mc<BM, NT, VA>(a, p.A, p.lda, m0, p.M, k0, p.K);
-    if constexpr (TB) load_mc<BN, NT, VB>(b, p.B, p.ldb, n0, p.N, k0, p.K);
-    else load_kc<BN, NT>(b, p.B, p.ldb, n0, p.N, k0, p.K);
+    la.load(sA + stage * kBK * RSA, kt);
+    lb.load(sB + stage * kBK * RSB, kt);
   };
 
   float acc[8][8];

@@ -1,0 +1,8 @@
+// fp64 DMMA GEMM, configuration 16: CTA 64x64x16, warps 2x2, 4 stages, MC layout mode 2.
+#include "gemm_f64_kernel.cuh"
+
+namespace rectri_cu {
+void dgemm_cfg16(const GemmParams<double>& p, bool ta, bool tb, bool vec2, cudaStream_t s) {
+  dgemm::Config<64, 64, 16, 2, 2, 4, 2>::run(p, ta, tb, vec2, s);
+}
+}  // namespace rectri_cu

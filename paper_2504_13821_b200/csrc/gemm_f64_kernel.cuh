@@ -40,42 +40,86 @@ __device__ __forceinline__ void dmma1684(double (&c)[4], double a0, double a1, d
 //   MC: outer-contiguous source, element (o, k) at X[o + k*ld]; rows = k.
 //   KC: k-contiguous source, element (o, k) at X[k + o*ld]; rows = o.
 // Out-of-range elements are zero-filled by the cp.async src-size operand.
-template <int BO, int BK, int NT, int VEC, bool KC>
+// Shared layout of an outer-contiguous (MC) tile: rows = k of BO doubles.
+//   MCMODE 0: 16-byte-chunk XOR swizzle, one warp copies one row.
+//   MCMODE 1: no swizzle, rows padded by 4 doubles (fragment reads stay
+//             conflict-free: double-bank = 4t + g), one warp copies one row.
+//   MCMODE 2: XOR swizzle, one warp copies 4 rows x 128 bytes.
+// k-contiguous (KC) tiles: rows = outer, kBK doubles, XOR swizzle.
+template <int BO, int MCMODE>
+struct McLayout {
+  static constexpr int STRIDE = MCMODE == 1 ? BO + 4 : BO;
+  __host__ __device__ static constexpr int elems(int rows) { return rows * STRIDE; }
+  __device__ static int idx(int row, int col) {
+    return MCMODE == 1 ? row * STRIDE + col : swz64(row, col, BO);
+  }
+};
+
+template <int BO, int BK, int NT, int VEC, bool KC, int MCMODE>
 struct TileLoader {
   static constexpr int kBK = BK;
-  static constexpr int WIDTH = KC ? kBK : BO;  // shared row width (doubles)
+  static constexpr int WIDTH = KC ? kBK : BO;  // logical row width (doubles)
   static constexpr int CPR = WIDTH / VEC;
   static constexpr int ROWS = KC ? BO : kBK;
   static constexpr int IT = CPR * ROWS / NT;
-  static constexpr int ROW_STEP = NT / CPR;
-  static_assert(NT % CPR == 0 && (CPR * ROWS) % NT == 0, "loader trip count");
+  static_assert(NT % CPR == 0 || (!KC && MCMODE == 2), "loader trip count");
+  static_assert((CPR * ROWS) % NT == 0, "loader trip count");
+  // MCMODE 2: a warp covers RPW rows x G chunks (G chunks = 128 bytes).
+  static constexpr int G = 128 / (8 * VEC);
+  static constexpr int RPW = 32 / G;
 
-  const double* base;  // X at the tile's outer origin o0
-  i64 ld;
+  const double* base;  // X at the tile's outer origin o0 (valid dummy source)
+  const double* p0;    // this thread's first chunk for k-tile 0
+  i64 ld, step;        // leading dimension; global stride between its chunks
   int row0, col;       // thread's first shared row, its chunk column (elements)
   int o_lim, k_lim;    // outer extent left from o0, and K
+  int fix_bytes;       // KC: per-row (outer) validity; MC: bytes of its column
+
+  // rows advanced per iteration
+  static constexpr int ROW_STEP = (!KC && MCMODE == 2) ? RPW * (NT / 32) / (CPR / G) : NT / CPR;
 
   __device__ void init(const double* X, i64 ld_, i64 o0, i64 O, i64 K) {
     ld = ld_;
-    row0 = threadIdx.x / CPR;
-    col = (threadIdx.x % CPR) * VEC;
+    if (!KC && MCMODE == 2) {
+      const int q = threadIdx.x;  // chunk id -> (row, chunk) in RPW x G warp tiles
+      const int lane = q & 31, w = q >> 5;
+      const int tiles_per_row = CPR / G;
+      const int tr = w / tiles_per_row, tc = w % tiles_per_row;
+      row0 = RPW * tr + lane / G;
+      col = (tc * G + lane % G) * VEC;
+    } else {
+      row0 = threadIdx.x / CPR;
+      col = (threadIdx.x % CPR) * VEC;
+    }
     o_lim = static_cast<int>(O - o0 < (1 << 30) ? O - o0 : (1 << 30));
     k_lim = static_cast<int>(K < (1 << 30) ? K : (1 << 30));
     base = KC ? X + o0 * ld : X + o0;
+    // Both layouts: element (row, col) of the tile at base + row*ld + col
+    // (KC: row = outer, col = k; MC: row = k, col = outer).
+    p0 = base + static_cast<i64>(row0) * ld + col;
+    step = static_cast<i64>(ROW_STEP) * ld;
+    if (!KC) {
+      const int rem = o_lim - col;
+      fix_bytes = rem >= VEC ? VEC * 8 : (rem > 0 ? rem * 8 : 0);
+    }
   }
 
   __device__ __forceinline__ void load(uint32_t stage, i64 kt) const {
     const int k0 = static_cast<int>(kt * kBK);
+    const double* tb = p0 + (KC ? static_cast<i64>(k0) : static_cast<i64>(k0) * ld);
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int row = row0 + it * ROW_STEP;
-      const int o = KC ? row : col;
-      const int k = k0 + (KC ? col : row);
-      const int rem = KC ? k_lim - k : o_lim - o;
-      const bool in = KC ? o < o_lim : k < k_lim;
-      const int bytes = in ? (rem >= VEC ? VEC * 8 : (rem > 0 ? rem * 8 : 0)) : 0;
-      const double* g = bytes ? (KC ? base + o * ld + k : base + o + static_cast<i64>(k) * ld) : base;
-      const uint32_t dst = stage + 8u * static_cast<uint32_t>(swz64(row, col, WIDTH));
+      int bytes;
+      if (KC) {
+        const int rem = k_lim - (k0 + col);
+        bytes = row < o_lim ? (rem >= VEC ? VEC * 8 : (rem > 0 ? rem * 8 : 0)) : 0;
+      } else {
+        bytes = (k0 + row < k_lim) ? fix_bytes : 0;
+      }
+      const double* g = bytes ? tb + it * step : base;
+      const int e = KC ? swz64(row, col, kBK) : McLayout<BO, MCMODE>::idx(row, col);
+      const uint32_t dst = stage + 8u * static_cast<uint32_t>(e);
       if constexpr (VEC == 2)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(g), "r"(bytes));
       else
@@ -84,7 +128,8 @@ struct TileLoader {
   }
 };
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TA, bool TB, int VEC>
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TA, bool TB, int VEC,
+          int MCMODE>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
     dgemm_dmma_kernel(const GemmParams<double> p) {
   constexpr int kBK = BK;
@@ -93,7 +138,10 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
   constexpr int TM = WM / 16, TN = WN / 8;
   constexpr int KK = kBK / 4;
   static_assert(WM % 16 == 0 && WN % 8 == 0, "warp tile");
-  constexpr uint32_t A_STAGE = BM * kBK * 8, B_STAGE = BN * kBK * 8;
+  using LA = McLayout<BM, MCMODE>;
+  using LB = McLayout<BN, MCMODE>;
+  constexpr uint32_t A_STAGE = (TA ? BM * kBK : LA::elems(kBK)) * 8;
+  constexpr uint32_t B_STAGE = (TB ? LB::elems(kBK) : BN * kBK) * 8;
 
   extern __shared__ __align__(128) double smem[];
   const uint32_t sA = smem_u32(smem);
@@ -106,8 +154,8 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
   const i64 n0 = static_cast<i64>(blockIdx.y) * BN;
   const i64 KT = ceil_div(p.K, kBK);
 
-  TileLoader<BM, BK, NT, VEC, TA> la;
-  TileLoader<BN, BK, NT, VEC, !TB> lb;
+  TileLoader<BM, BK, NT, VEC, TA, MCMODE> la;
+  TileLoader<BN, BK, NT, VEC, !TB, MCMODE> lb;
   la.init(p.A, p.lda, m0, p.M, p.K);
   lb.init(p.B, p.ldb, n0, p.N, p.K);
 
@@ -120,22 +168,22 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int m = wm0 + 16 * i + 8 * h + g;
-      a_off[i][h] = 8u * static_cast<uint32_t>(TA ? swz64(m, t, kBK) : swz64(t, m, BM));
+      a_off[i][h] = 8u * static_cast<uint32_t>(TA ? swz64(m, t, kBK) : LA::idx(t, m));
     }
 #pragma unroll
   for (int j = 0; j < TN; ++j) {
     const int n = wn0 + 8 * j + g;
-    b_off[j] = 8u * static_cast<uint32_t>(TB ? swz64(t, n, BN) : swz64(n, t, kBK));
+    b_off[j] = 8u * static_cast<uint32_t>(TB ? LB::idx(t, n) : swz64(n, t, kBK));
   }
   // k-major layouts: a k-step moves 4 rows and keeps (row & 3), hence the
   // swizzle; k-contiguous layouts recompute the swizzled column.
   auto a_addr = [&](uint32_t stage, int i, int h, int kk) -> uint32_t {
-    if constexpr (!TA) return stage + a_off[i][h] + static_cast<uint32_t>(kk * 4 * BM * 8);
+    if constexpr (!TA) return stage + a_off[i][h] + static_cast<uint32_t>(kk * 4 * LA::STRIDE * 8);
     const int m = wm0 + 16 * i + 8 * h + g;
     return stage + 8u * static_cast<uint32_t>(swz64(m, kk * 4 + t, kBK));
   };
   auto b_addr = [&](uint32_t stage, int j, int kk) -> uint32_t {
-    if constexpr (TB) return stage + b_off[j] + static_cast<uint32_t>(kk * 4 * BN * 8);
+    if constexpr (TB) return stage + b_off[j] + static_cast<uint32_t>(kk * 4 * LB::STRIDE * 8);
     const int n = wn0 + 8 * j + g;
     return stage + 8u * static_cast<uint32_t>(swz64(n, kk * 4 + t, kBK));
   };
@@ -226,12 +274,13 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
 
 // Host launcher of one configuration (all four transpose forms, both copy
 // widths); instantiated in gemm_f64_cfg*.cu.
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MCMODE = 0>
 struct Config {
   template <bool TA, bool TB, int VEC>
   static void launch(const GemmParams<double>& p, cudaStream_t s) {
-    auto kern = dgemm_dmma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TA, TB, VEC>;
-    constexpr int smem = STAGES * (BM + BN) * BK * static_cast<int>(sizeof(double));
+    auto kern = dgemm_dmma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TA, TB, VEC, MCMODE>;
+    constexpr int pad = MCMODE == 1 ? 4 : 0;
+    constexpr int smem = STAGES * (BM + BN + 2 * pad) * BK * static_cast<int>(sizeof(double));
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
     kern<<<grid, WARPS_M * WARPS_N * 32, smem, s>>>(p);
@@ -271,7 +320,9 @@ using DgemmRun = void (*)(const GemmParams<double>&, bool, bool, bool, cudaStrea
   X(11, 64, 64, 16, 2, 2, 3)             \
   X(12, 64, 128, 16, 2, 2, 4)            \
   X(13, 128, 64, 16, 2, 2, 4)            \
-  X(14, 64, 64, 16, 2, 1, 4)
+  X(14, 64, 64, 16, 2, 1, 4)             \
+  X(15, 64, 64, 16, 2, 2, 4)             \
+  X(16, 64, 64, 16, 2, 2, 4)
 #define RECTRI_DECL(ID, BM, BN, BK, WM, WN, ST) \
   void dgemm_cfg##ID(const GemmParams<double>&, bool, bool, bool, cudaStream_t);
 RECTRI_DGEMM_CONFIGS(RECTRI_DECL)

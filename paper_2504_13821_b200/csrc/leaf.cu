@@ -197,24 +197,25 @@ struct LeafSmem {
 
 // The blocks of L' a CTA consumes, in order: for each row block I (ascending
 // for TRSM, descending for TRMM) its off-diagonal blocks J = 0 .. I-1, then
-// its diagonal block.  Element s of that sequence -> (I, J), J == I meaning
-// the diagonal block.
-__device__ __forceinline__ void seq_block(int s, int nblk, bool ascending, int& I, int& J) {
-  // Row block order index q has q+1 elements (q off-diagonal + 1 diagonal)
-  // when ascending (I = q), or I+1 elements with I = nblk-1-q otherwise.
-  int q = 0, base = 0;
-  while (true) {
-    const int Iq = ascending ? q : nblk - 1 - q;
-    const int len = Iq + 1;
-    if (s < base + len) {
-      I = Iq;
-      J = s - base;
-      return;
-    }
-    base += len;
-    ++q;
+// its diagonal block (J == I).
+struct SeqCursor {
+  int I, J, nblk;
+  bool asc;
+  __device__ void start(int nblk_, bool asc_) {
+    nblk = nblk_;
+    asc = asc_;
+    I = asc ? 0 : nblk - 1;
+    J = 0;
   }
-}
+  __device__ void next() {
+    if (J < I) {
+      ++J;
+    } else {
+      I += asc ? 1 : -1;
+      J = 0;
+    }
+  }
+};
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
@@ -261,33 +262,52 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
     return;
   }
 
-  // Staging of sequence element s into its ring slot.  Off-diagonal blocks
-  // are stored k-major for the GEMM part (each warp copies 4 k x 8 rows);
-  // the diagonal block as [p][r] = L'(r, p) for p < r, zero elsewhere.
-  // Masked / out-of-range entries are zero-filled (never read).
-  const int nseq = nblk * (nblk + 1) / 2;
-  auto stage = [&](int s) {
-    int I, J;
-    seq_block(s, nblk, asc, I, J);
-    T* dst = ring + (s % kRing) * LeafSmem<T>::blk;
-    const bool diag = I == J;
-    const int r0 = I * kRB, j0 = J * kRB;
+  // Staging of a block of L' into a ring slot.  L'(r, j) is affine in the
+  // thread's local (r, j): address = base(I, J) + sgn * (r_l * sr + j_l * sj)
+  // with strides +-1 / +-lda, so each thread's 4 element offsets are
+  // computed once.  Off-diagonal blocks are stored k-major for the GEMM part
+  // (each warp copies 4 k x 8 rows); the diagonal block as [p][r] = L'(r, p)
+  // for p < r, zero elsewhere.  Masked entries are zero-filled (never read).
+  constexpr int kPer = kRB * kRB / kThreads;  // elements per thread per block
+  const i64 sr = p.swapped ? p.lda : 1, sj = p.swapped ? 1 : p.lda;
+  const i64 sgn = p.reflected ? -1 : 1;
+  i64 off_o[kPer], off_d[kPer];
+  int so_o[kPer], so_d[kPer];  // shared element offsets within a slot
+  int rl_o[kPer], rl_d[kPer];
+  bool lower_d[kPer];
 #pragma unroll
-    for (int it = 0; it < kRB * kRB / kThreads; ++it) {
-      const int q = tid + it * kThreads;
-      const int w = q >> 5, l = q & 31;
-      int r, j;
-      if (diag) {
-        r = l;
-        j = w;
-      } else {
-        r = 8 * (w & 3) + (l >> 2);
-        j = 4 * (w >> 2) + (l & 3);
+  for (int it = 0; it < kPer; ++it) {
+    const int q = tid + it * kThreads;
+    const int w = q >> 5, l = q & 31;
+    int r = 8 * (w & 3) + (l >> 2), j = 4 * (w >> 2) + (l & 3);
+    off_o[it] = sgn * (r * sr + j * sj);
+    so_o[it] = L::lblk(r, j);
+    rl_o[it] = r;
+    r = l;
+    j = w;
+    off_d[it] = sgn * (r * sr + j * sj);
+    so_d[it] = j * kRB + r;
+    rl_d[it] = r;
+    lower_d[it] = j < r;
+  }
+  auto stage = [&](int I, int J, int slot) {
+    T* dst = ring + slot * LeafSmem<T>::blk;
+    const int r0 = I * kRB, j0 = J * kRB;
+    const i64 rr = p.reflected ? n - 1 - r0 : r0;
+    const i64 jj = p.reflected ? n - 1 - j0 : j0;
+    const T* base = p.A + rr * sr + jj * sj;
+    if (I != J) {
+#pragma unroll
+      for (int it = 0; it < kPer; ++it) {
+        const bool ok = r0 + rl_o[it] < n;
+        cp_async_elem(dst + so_o[it], ok ? base + off_o[it] : p.A, ok);
       }
-      const int gr = r0 + r, gj = j0 + j;
-      const bool ok = gr < n && (diag ? j < r : true);
-      T* sdst = diag ? dst + j * kRB + r : dst + L::lblk(r, j);
-      cp_async_elem(sdst, ok ? lprime_ptr(p, gr, gj) : p.A, ok);
+    } else {
+#pragma unroll
+      for (int it = 0; it < kPer; ++it) {
+        const bool ok = lower_d[it] && r0 + rl_d[it] < n;
+        cp_async_elem(dst + so_d[it], ok ? base + off_d[it] : p.A, ok);
+      }
     }
   };
 
@@ -299,9 +319,16 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
     cp_async_elem(panel + L::panel(r, c), ok ? p.B + gaddr(r, c) : p.B, ok);
   }
   cp_async_commit();
+  const int nseq = nblk * (nblk + 1) / 2;
+  SeqCursor prod, cons;  // producer runs kRing - 1 elements ahead
+  prod.start(nblk, asc);
+  cons.start(nblk, asc);
 #pragma unroll
   for (int s = 0; s < kRing - 1; ++s) {
-    if (s < nseq) stage(s);
+    if (s < nseq) {
+      stage(prod.I, prod.J, s % kRing);
+      prod.next();
+    }
     cp_async_commit();
   }
   for (int r = tid; r < rows_p; r += kThreads) {
@@ -331,14 +358,16 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
   const int gq = lane & 7;
   const bool neg = p.trsm != 0;
 
-  for (int s = 0; s < nseq; ++s) {
+  for (int s = 0; s < nseq; ++s, cons.next()) {
     cp_async_wait<kRing - 2>();  // element s has landed (this thread's copies)
     __syncthreads();              // ... everyone's; slot (s-1) % kRing is free
-    if (s + kRing - 1 < nseq) stage(s + kRing - 1);
+    if (s + kRing - 1 < nseq) {
+      stage(prod.I, prod.J, (s + kRing - 1) % kRing);
+      prod.next();
+    }
     cp_async_commit();
 
-    int I, J;
-    seq_block(s, nblk, asc, I, J);
+    const int I = cons.I, J = cons.J;
     const int r0 = I * kRB;
     const uint32_t slot = ring_u32 + static_cast<uint32_t>((s % kRing) * LeafSmem<T>::blk * sizeof(T));
     if (J == 0) {  // first element of row block I: fresh accumulators

@@ -26,14 +26,15 @@ if kind in ("trsm", "trmm"):
     rc.fill_uniform(B.view(), seed=2)
     fn = rc.rec_trsm if kind == "trsm" else rc.rec_trmm
     fn(TriangularSpec(), A.cview(), B.view(), Threshold(t), be)
-elif kind == "gemm":
+elif kind in ("gemm", "gemmtn"):
     M, N, K = args
-    A = MatrixBuffer(M, K, f64, "cuda")
+    ta = Trans.Trans if kind == "gemmtn" else Trans.NoTrans
+    A = MatrixBuffer(K, M, f64, "cuda") if kind == "gemmtn" else MatrixBuffer(M, K, f64, "cuda")
     B = MatrixBuffer(K, N, f64, "cuda")
     C = MatrixBuffer(M, N, f64, "cuda")
     for i, x in enumerate((A, B, C)):
         rc.fill_uniform(x.view(), seed=i)
-    rc.gemm(-1.0, Trans.NoTrans, A.cview(), Trans.NoTrans, B.cview(), 1.0, C.view(), be)
+    rc.gemm(-1.0, ta, A.cview(), Trans.NoTrans, B.cview(), 1.0, C.view(), be)
 elif kind == "leaf":
     nb, m = args
     A = MatrixBuffer(nb, nb, f64, "cuda")
