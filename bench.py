@@ -417,29 +417,34 @@ def main():
 
 
 def cublas_compare(A, B0, n, m, args):
-    """cuBLAS dtrsm (torch.linalg.solve_triangular) and dgemm (torch.mm) on
-    the same device inputs, as a reported comparison only."""
-    out = {}
-    Am = A.data.t()  # (n, n) logical matrix view
-    L = torch.tril(Am)
-    Bm = B0.data.t()
+    """cuBLAS dtrsm / dtrmm / dgemm on the SAME device inputs (reported
+    comparison only; tools/libcublas_cmp.so, best of 2 with CUDA events).
+    cuBLAS trmm is out of place (C = A B); flops counted like ours (n^2 m)."""
+    import ctypes
+
+    lib = ctypes.CDLL(str(ROOT / "tools" / "libcublas_cmp.so"))
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    lib.cmp_dtrsm_lln.argtypes = [vp, i64, vp, i64, ctypes.c_int]
+    lib.cmp_dtrmm_lun.argtypes = [vp, i64, vp, vp, i64, ctypes.c_int]
+    lib.cmp_dgemm.argtypes = [vp, vp, vp, i64, ctypes.c_int]
+    for f in (lib.cmp_dtrsm_lln, lib.cmp_dtrmm_lun, lib.cmp_dgemm):
+        f.restype = ctypes.c_double
+    work = B0.data.clone()
+    out = torch.empty_like(work)
     torch.cuda.synchronize()
-    for name, fn in (("dtrsm_LLN", lambda: torch.linalg.solve_triangular(L, Bm, upper=False)),
-                     ("dgemm", lambda: torch.mm(L, Bm))):
-        fn()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        r = fn()
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        fl = float(n) * n * m * (2 if name == "dgemm" else 1)
-        out[name] = {"ms": ms, "gflops": fl / ms / 1e6, "flops_counted": "2n^2m" if name == "dgemm" else "n^2m"}
-        del r
-    del L
+    # trsm solves in place: each timed call re-solves the previous solution,
+    # which changes values but not the work.
+    t_trsm = lib.cmp_dtrsm_lln(A.data.data_ptr(), n, work.data_ptr(), m, 2)
+    work.copy_(B0.data)
+    t_trmm = lib.cmp_dtrmm_lun(A.data.data_ptr(), n, work.data_ptr(), out.data_ptr(), m, 2)
+    res = {"dtrsm_LLN": {"ms": t_trsm, "gflops": float(n) * n * m / t_trsm / 1e6},
+           "dtrmm_LUN": {"ms": t_trmm, "gflops": float(n) * n * m / t_trmm / 1e6, "note": "out of place"}}
+    if m == n:
+        t_gemm = lib.cmp_dgemm(A.data.data_ptr(), work.data_ptr(), out.data_ptr(), n, 2)
+        res["dgemm"] = {"ms": t_gemm, "tflops_2n3": 2.0 * n ** 3 / t_gemm / 1e9}
+    del work, out
     torch.cuda.empty_cache()
-    return out
+    return res
 
 
 def cpu_baseline(args):

@@ -86,6 +86,20 @@ def build(verbose: bool = False) -> Path:
     return LIB
 
 
+CMP_SRC = ROOT / "tools" / "cublas_cmp.cu"
+CMP_LIB = ROOT / "tools" / "libcublas_cmp.so"
+
+
+def build_cublas_cmp() -> Path:
+    """The cuBLAS comparison shim used by bench.py (reported comparison only)."""
+    if _stale(CMP_LIB, [CMP_SRC]):
+        cmd = [nvcc(), *ARCH, "-O2", "-Xcompiler", "-fPIC", "-shared", str(CMP_SRC), "-o", str(CMP_LIB), "-lcublas"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"cublas_cmp failed to build:\n{r.stderr}")
+    return CMP_LIB
+
+
 EXAMPLE_SRC = ROOT / "tests" / "cpp" / "dropin_example.cpp"
 EXAMPLE_BIN = ROOT / "tests" / "cpp" / "build" / "dropin_example"
 
@@ -108,4 +122,5 @@ def build_dropin_example() -> Path:
 if __name__ == "__main__":
     build(verbose=True)
     build_dropin_example()
+    build_cublas_cmp()
     sys.exit(0)

@@ -117,6 +117,8 @@ struct TileLoader {
       } else {
         bytes = (k0 + row < k_lim) ? fix_bytes : 0;
       }
+      // Hoisted per-thread pointer: k*ld would otherwise be a 64-bit multiply
+      // per chunk and k-tile on outer-contiguous tiles.
       const double* g = bytes ? tb + it * step : base;
       const int e = KC ? swz64(row, col, kBK) : McLayout<BO, MCMODE>::idx(row, col);
       const uint32_t dst = stage + 8u * static_cast<uint32_t>(e);

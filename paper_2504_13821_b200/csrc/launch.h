@@ -43,6 +43,7 @@ struct LeafParams {
   int unit;
   int trsm;  // 1: solve, 0: multiply
   T alpha;
+  int debug_skip = 0;  // timing experiments only (RECTRI_CU_LEAF_DEBUG): 1 no diag part, 2 no GEMM part
 };
 
 constexpr int kLeafMax = 256;

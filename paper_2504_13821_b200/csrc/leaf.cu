@@ -26,6 +26,8 @@
 // The per-element arithmetic order depends only on the tile, never on the
 // number of right-hand sides, so results are bitwise independent of how the
 // right-hand sides are sharded.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -234,31 +236,39 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
   const int ncols = static_cast<int>(min(static_cast<i64>(kNC), p.nrhs - c0));
   const bool asc = p.trsm != 0;  // TRMM runs bottom-up (in place)
 
-  auto gaddr = [&](int r, int c) -> i64 {  // global offset of B'(r, c0 + c)
-    const i64 sr = p.reflected ? n - 1 - r : r;
-    return p.right ? sr * p.ldb + c0 + c : (c0 + c) * p.ldb + sr;
-  };
-  // Panel element assignment: Left -> each warp covers 4 rows x 8 rhs
-  // (32-byte global sectors); Right -> each warp covers 32 rhs of one row.
-  auto panel_rc = [&](int q, int& r, int& c) {
-    if (p.right) {
-      r = q / kNC;
-      c = q % kNC;
+  // Visits every panel element (r < rows_p, c < kNC) once per thread set,
+  // with its global pointer (valid only when r < n && c < ncols):
+  //   Left  -> each warp covers 4 rows x 8 right-hand sides (32-byte global
+  //            sectors); the thread's 4 column pointers are fixed.
+  //   Right -> each warp covers the 32 right-hand sides of one row.
+  // No divisions, no 64-bit multiplies per element.
+  const i64 rstep = p.reflected ? -1 : 1;  // global row step for r -> r + 1 (Left)
+  auto for_panel = [&](auto&& f) {
+    if (!p.right) {
+      const int rl = lane & 3, cl = lane >> 2;
+#pragma unroll
+      for (int cg = 0; cg < kNC / 8; ++cg) {
+        const int c = 8 * cg + cl;
+        const T* colp = p.B + (c0 + c) * p.ldb + (p.reflected ? n - 1 : 0);
+        for (int rt = warp; rt < rows_p / 4; rt += kThreads / 32) {
+          const int r = 4 * rt + rl;
+          f(r, c, colp + r * rstep);
+        }
+      }
     } else {
-      const int w = q >> 5, l = q & 31;
-      const int row_tiles = rows_p / 4;
-      r = 4 * (w % row_tiles) + (l & 3);
-      c = 8 * (w / row_tiles) + (l >> 2);
+      const int c = lane;
+      for (int r = warp; r < rows_p; r += kThreads / 32) {
+        const i64 sr = p.reflected ? n - 1 - r : r;
+        f(r, c, p.B + sr * p.ldb + c0 + c);
+      }
     }
   };
 
   // TRMM with alpha == 0 writes zeros without reading B (base_kernels.cpp:143-150).
   if (!p.trsm && p.alpha == T(0)) {
-    for (int q = tid; q < rows_p * kNC; q += kThreads) {
-      int r, c;
-      panel_rc(q, r, c);
-      if (r < n && c < ncols) p.B[gaddr(r, c)] = T(0);
-    }
+    for_panel([&](int r, int c, const T* g) {
+      if (r < n && c < ncols) *const_cast<T*>(g) = T(0);
+    });
     return;
   }
 
@@ -312,12 +322,10 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
   };
 
   // 1. Panel load + the first ring elements (one commit group each).
-  for (int q = tid; q < rows_p * kNC; q += kThreads) {
-    int r, c;
-    panel_rc(q, r, c);
+  for_panel([&](int r, int c, const T* g) {
     const bool ok = r < n && c < ncols;
-    cp_async_elem(panel + L::panel(r, c), ok ? p.B + gaddr(r, c) : p.B, ok);
-  }
+    cp_async_elem(panel + L::panel(r, c), ok ? g : p.B, ok);
+  });
   cp_async_commit();
   const int nseq = nblk * (nblk + 1) / 2;
   SeqCursor prod, cons;  // producer runs kRing - 1 elements ahead
@@ -342,11 +350,7 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
   cp_async_wait<kRing - 1>();  // the panel group
   __syncthreads();
   if (p.trsm && p.alpha != T(1)) {  // x = alpha * b (base_kernels.cpp:76-77)
-    for (int q = tid; q < rows_p * kNC; q += kThreads) {
-      int r, c;
-      panel_rc(q, r, c);
-      panel[L::panel(r, c)] *= p.alpha;
-    }
+    for_panel([&](int r, int c, const T*) { panel[L::panel(r, c)] *= p.alpha; });
   }
 
   typename GemmPartOf<T>::type gp;
@@ -375,7 +379,7 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
       else gp.zero();
     }
     if (J < I) {  // 2. off-diagonal block-row GEMM
-      gp.mma(slot, panel_u32, J * kRB);
+      if (p.debug_skip != 2) gp.mma(slot, panel_u32, J * kRB);
       continue;
     }
     // 3. diagonal block (slot holds ld[p * 32 + r] = L'(r, p), p < r).
@@ -383,16 +387,21 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
     if (p.trsm) gp.store(panel, r0, neg);
     else gp.store(ys, 0, false);
     __syncthreads();
+    if (p.debug_skip == 1) continue;
     T v[4];
     if (p.trsm) {
+      T rv[4];  // reciprocal diagonal of this thread's rows, off the chain
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = panel[L::panel(r0 + gq + 8 * q, cc)];
+      for (int q = 0; q < 4; ++q) {
+        v[q] = panel[L::panel(r0 + gq + 8 * q, cc)];
+        rv[q] = dg[r0 + gq + 8 * q];
+      }
 #pragma unroll
       for (int pp = 0; pp < kRB; ++pp) {
         const int qo = pp >> 3, go = pp & 7;
         T x = T(0);
         if (gq == go) {
-          v[qo] = v[qo] * dg[r0 + pp];
+          v[qo] = v[qo] * rv[qo];
           x = v[qo];
         }
         x = __shfl_sync(0xffffffffu, x, (lane & ~7) | go);
@@ -426,16 +435,24 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
   __syncthreads();
 
   // 4. Write back.
-  for (int q = tid; q < rows_p * kNC; q += kThreads) {
-    int r, c;
-    panel_rc(q, r, c);
-    if (r < n && c < ncols) p.B[gaddr(r, c)] = panel[L::panel(r, c)];
-  }
+  for_panel([&](int r, int c, const T* g) {
+    if (r < n && c < ncols) *const_cast<T*>(g) = panel[L::panel(r, c)];
+  });
+}
+
+int leaf_debug() {
+  static int v = [] {
+    const char* e = getenv("RECTRI_CU_LEAF_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
 }
 
 template <typename T>
-void launch_leaf(const LeafParams<T>& p, cudaStream_t s) {
-  if (p.n <= 0 || p.nrhs <= 0) return;
+void launch_leaf(const LeafParams<T>& p_in, cudaStream_t s) {
+  if (p_in.n <= 0 || p_in.nrhs <= 0) return;
+  LeafParams<T> p = p_in;
+  p.debug_skip = leaf_debug();
   const int smem = static_cast<int>(LeafSmem<T>::total * sizeof(T));
   cudaFuncSetAttribute(leaf_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const unsigned grid = static_cast<unsigned>(ceil_div(p.nrhs, kNC));

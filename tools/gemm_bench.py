@@ -15,10 +15,10 @@ N = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
 be = Backend.cuda(flags=NO_GRAPH)
 res = []
 for MK in (8192, 4096, 2048, 1024, 512, 256, 128, 64):
-    for ta, tb, tag in ((0, 0, "NN"), (1, 0, "TN")):
+    for ta, tb, tag in ((0, 0, "NN"), (1, 0, "TN"), (0, 1, "NT")):
         M = K = MK
         A = MatrixBuffer(K if ta else M, M if ta else K, dt, "cuda")
-        B = MatrixBuffer(K, N, dt, "cuda")
+        B = MatrixBuffer(N, K, dt, "cuda") if tb else MatrixBuffer(K, N, dt, "cuda")
         C = MatrixBuffer(M, N, dt, "cuda")
         for i, x in enumerate((A, B, C)):
             rc.fill_uniform(x.view(), seed=i)
