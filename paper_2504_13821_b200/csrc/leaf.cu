@@ -407,23 +407,34 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
         x = __shfl_sync(0xffffffffu, x, (lane & ~7) | go);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
+          // Branch-free: the shared load is unconditional (always in range;
+          // zero for r <= pp) so it pipelines; the update is selected, so a
+          // masked entry never reaches v even when x is not finite.
           const int r = gq + 8 * q;
-          if (r > pp) v[q] = fma(-ld[pp * kRB + r], x, v[q]);
+          const T nv = fma(-ld[pp * kRB + r], x, v[q]);
+          v[q] = r > pp ? nv : v[q];
         }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) panel[L::panel(r0 + gq + 8 * q, cc)] = v[q];
     } else {
+      T dr[4];  // diagonal of this thread's rows (1 for Unit)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = ys[L::panel(gq + 8 * q, cc)];
-#pragma unroll 8
+      for (int q = 0; q < 4; ++q) {
+        v[q] = ys[L::panel(gq + 8 * q, cc)];
+        dr[q] = dg[r0 + gq + 8 * q];
+      }
+#pragma unroll
       for (int pp = 0; pp < kRB; ++pp) {
         const T b = panel[L::panel(r0 + pp, cc)];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
+          // Branch-free masked product (see the TRSM loop): p < r uses L',
+          // p == r the diagonal, p > r is skipped by selection.
           const int r = gq + 8 * q;
-          if (pp < r) v[q] = fma(ld[pp * kRB + r], b, v[q]);
-          else if (pp == r) v[q] = fma(dg[r0 + r], b, v[q]);
+          const T coef = pp == r ? dr[q] : ld[pp * kRB + r];
+          const T nv = fma(coef, b, v[q]);
+          v[q] = pp <= r ? nv : v[q];
         }
       }
       __syncwarp();  // all readers of column cc live in this warp
