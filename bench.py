@@ -172,7 +172,7 @@ def run_reference(args, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, world),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -198,8 +198,9 @@ def make_host_inputs(n, m, op):
 
 
 def workload_config(args, world):
+    tag = ("C5 tall-RHS" if args.config == "c5" else "C3") + f" ({args.op_headline} headline)"
     return {
-        "workload": (f"C3 ({args.op_headline} headline): TRSM Left/Lower/NoTrans/NonUnit + TRMM Left/Upper/NoTrans "
+        "workload": (f"{tag}: TRSM Left/Lower/NoTrans/NonUnit + TRMM Left/Upper/NoTrans "
                      f"fp64, n={args.n}, m={args.m} per GPU (m={args.m * world} total), alpha=1, "
                      "diagonally dominant random A"),
         "n": args.n, "m_per_gpu": args.m, "m_total": args.m * world, "threshold": args.threshold,
@@ -216,8 +217,11 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=16384)
-    ap.add_argument("--m", type=int, default=16384, help="right-hand sides per GPU")
+    ap.add_argument("--config", choices=["c3", "c5"], default="c3",
+                    help="c3: n=m=16384 per GPU (weak scaling); c5: tall RHS n=8192, m=524288 total (strong)")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--m", type=int, default=None, help="right-hand sides per GPU")
+    ap.add_argument("--no-fp32", action="store_true")
     ap.add_argument("--threshold", type=int, default=256)
     ap.add_argument("--op-headline", choices=["trsm", "trmm"], default="trsm")
     ap.add_argument("--ref-cols", type=int, default=256)
@@ -230,6 +234,14 @@ def main():
     args = ap.parse_args()
 
     world, rank, local = setup_dist(args)
+    if args.config == "c5":
+        args.n = args.n or 8192
+        args.m = args.m or 524288 // world
+        args.scaling = "strong"
+    else:
+        args.n = args.n or 16384
+        args.m = args.m or 16384
+        args.scaling = "weak"
     if args.impl == "reference":
         run_reference(args, world, rank)
         if world > 1:
@@ -267,27 +279,31 @@ def main():
     }
     flops_per_gpu = float(n) * n * m
 
-    def one(op):
+    def one(op, Abuf=None, Bbuf=None):
+        Abuf = Abuf if Abuf is not None else A
+        Bbuf = Bbuf if Bbuf is not None else B
         fn = rc.rec_trsm if op == "trsm" else rc.rec_trmm
         if world > 1:
-            dist.broadcast(A.data, src=0)
-        fn(specs[op], A.cview(), B.view(), Threshold(args.threshold), be)
+            dist.broadcast(Abuf.data, src=0)
+        fn(specs[op], Abuf.cview(), Bbuf.view(), Threshold(args.threshold), be)
 
-    def timed(op):
+    def timed(op, Abuf=None, Bbuf=None, B0buf=None):
+        Bbuf = Bbuf if Bbuf is not None else B
+        B0buf = B0buf if B0buf is not None else B0
         for _ in range(args.warmup):
-            B.data.copy_(B0.data)
-            one(op)
+            Bbuf.data.copy_(B0buf.data)
+            one(op, Abuf, Bbuf)
         rc.sync(stream)
         barrier(world)
         launches0 = rc.launch_count()
         evs = []
         with ClockSampler(local) as clk:
             for _ in range(args.steps):
-                B.data.copy_(B0.data)
+                Bbuf.data.copy_(B0buf.data)
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                one(op)
+                one(op, Abuf, Bbuf)
                 e1.record(stream)
                 evs.append((e0, e1))
             rc.sync(stream)
@@ -328,6 +344,27 @@ def main():
                 "workload": f"TRMM Left/Upper/NoTrans/NonUnit fp64 n={n}, m={m} per GPU"}
         log(f"trmm: {tv:.1f} GFLOP/s, {tms:.2f} ms/step")
 
+    # fp32 line: TRSM L/L/N/NU on the same inputs rounded to fp32.
+    fp32 = None
+    if not args.no_fp32:
+        A32 = MatrixBuffer(n, n, torch.float32, dev)
+        A32.data.copy_(A.data)
+        B32_0 = MatrixBuffer(n, m, torch.float32, dev)
+        B32_0.data.copy_(B0.data)
+        B32 = MatrixBuffer(n, m, torch.float32, dev)
+        v32, ms32, l32, clk32 = timed("trsm", A32, B32, B32_0)
+        fp32 = {"value": v32, "unit": "GFLOP/s", "ms_per_step": ms32, "gpu_launches": l32, "clocks": clk32,
+                "pct_of_ffma_peak": v32 / 1e3 / rc.probe_peak("f32") * 100,
+                "workload": f"TRSM Left/Lower/NoTrans/NonUnit fp32 n={n}, m={m} per GPU (FFMA path)"}
+        if not args.no_cublas and world == 1:
+            try:
+                fp32["cublas_strsm_LLN"] = cublas_strsm(A32, B32_0, n, m)
+            except Exception as e:  # pragma: no cover
+                fp32["cublas_strsm_LLN"] = {"error": str(e)}
+        log(f"fp32 trsm: {v32:.1f} GFLOP/s, {ms32:.2f} ms/step")
+        del A32, B32_0, B32
+        torch.cuda.empty_cache()
+
     # Per-kernel-class breakdown with CUDA events around every launch (one
     # extra untimed call, direct launches): the roofline's achieved figure.
     B.data.copy_(B0.data)
@@ -362,13 +399,14 @@ def main():
     # End to end through the C-ABI with pinned host buffers.
     e2e = None
     if not args.no_e2e:
+        me = min(m, 65536)  # pinned host budget: C5 uses a 65536-column slice per GPU
         Ah = torch.empty((n, n), dtype=f64, pin_memory=True)
         Ah.copy_(A.data)
-        Bh0 = torch.empty((m, n), dtype=f64, pin_memory=True)
-        Bh0.copy_(B0.data)
-        Bh = torch.empty((m, n), dtype=f64, pin_memory=True)
+        Bh0 = torch.empty((me, n), dtype=f64, pin_memory=True)
+        Bh0.copy_(B0.data[:me])
+        Bh = torch.empty((me, n), dtype=f64, pin_memory=True)
         Av = rc.MatrixView(Ah, n, n).as_const()
-        Bv = rc.MatrixView(Bh, n, m)
+        Bv = rc.MatrixView(Bh, n, me)
         be_sync = Backend.cuda(device=local, stream=stream)
         walls = []
         for i in range(args.warmup + args.steps):
@@ -380,8 +418,11 @@ def main():
             if i >= args.warmup:
                 walls.append(w)
         wall = allmax(sum(walls), world)
-        e2e = {"value": flops_per_gpu * world * args.steps / wall / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": (n * n + n * m) * 8 * world, "d2h_bytes_per_step": n * m * 8 * world,
+        e2e = {"value": float(n) * n * me * world * args.steps / wall / 1e9, "unit": "GFLOP/s",
+               # A: stored triangle as 512-column trapezoids (driver.cu copy_triangle_h2d)
+               "h2d_bytes_per_step": (sum((n - c0) * min(512, n - c0) for c0 in range(0, n, 512)) + n * me) * 8 * world,
+               "d2h_bytes_per_step": n * me * 8 * world,
+               "rhs_per_gpu": me,
                "ms_per_step": wall / args.steps * 1e3,
                "path": "rectri_cu_rec_trsm_f64 with pinned host views (H2D A+B, compute, D2H B), wall clock"}
         log(f"e2e: {e2e['value']:.1f} GFLOP/s")
@@ -402,13 +443,13 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated uniform[-1,1), dominant A)",
             "config": workload_config(args, world),
             "pct_of_peak": value / 1e3 / (peak64 * world) * 100,
             "residual": {"eta": eta, "finite": finite, "bound": 32,
                          "definition": "||tril(A) X - B||_max / (||A||_inf max(|X|,|B|,1) n eps), 8 sampled columns"},
-            "trmm": trmm, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "cublas": cublas,
+            "trmm": trmm, "fp32": fp32, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "cublas": cublas,
             "clocks": clocks, "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
@@ -445,6 +486,19 @@ def cublas_compare(A, B0, n, m, args):
     del work, out
     torch.cuda.empty_cache()
     return res
+
+
+def cublas_strsm(A32, B32_0, n, m):
+    """cuBLAS strsm (Left/Lower/N/NonUnit) on the same fp32 device inputs."""
+    import ctypes
+
+    lib = ctypes.CDLL(str(ROOT / "tools" / "libcublas_cmp.so"))
+    lib.cmp_strsm_lln.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]
+    lib.cmp_strsm_lln.restype = ctypes.c_double
+    work = B32_0.data.clone()
+    t = lib.cmp_strsm_lln(A32.data.data_ptr(), n, work.data_ptr(), m, 2)
+    del work
+    return {"ms": t, "gflops": float(n) * n * m / t / 1e6}
 
 
 def cpu_baseline(args):

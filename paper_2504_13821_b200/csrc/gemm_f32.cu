@@ -3,10 +3,16 @@
 // Replaces the reference's CPU GEMM (src/gemm.cpp:17-216; f32 microkernel
 // src/gemm_kernels_avx2.cpp:13-40) for fp32.  The north star keeps fp32 on
 // exact FFMA (TF32 would change the numerics), so this is a SIMT kernel:
-// CTA tile BM x BN x 16, each thread an 8 x 8 register tile (two 4x4
-// quadrants per dimension so fragment reads are 128-bit and conflict-free),
-// STAGES-deep cp.async ring.  Operands that are contiguous along k are
-// transposed on the fly by 4-byte cp.async into the k-major shared layout.
+// CTA tile BM x BN x 16, 256 threads, each an 8 x 8 register tile, STAGES-deep
+// cp.async ring.  The two operand layouts get their own shared layout and
+// fragment pattern:
+//   outer-contiguous source (A for op N, B for op T): shared [k][o], 16-byte
+//     copies; a thread's 8 outer indices are two runs of 4 (o = 4t.., BO/2+4t..)
+//     read as two LDS.128 per k;
+//   k-contiguous source (A for op T, B for op N): shared [o][k + 2], 8-byte
+//     copies (no transposition); a thread's 8 outer indices are t + 16j, read
+//     as LDS.64 pairs covering two k-steps (row stride 18 floats: the 16
+//     lanes of a phase hit distinct bank pairs).
 // Accumulation is a k-ascending fma chain per element, independent of the
 // tile configuration.
 #include "common.cuh"
@@ -16,47 +22,43 @@ namespace rectri_cu {
 namespace {
 
 constexpr int kBK = 16;
-constexpr int kPad = 4;  // floats of row padding (keeps 16-byte alignment)
+constexpr int kPadMC = 4;  // [k][o] rows: BO + 4 floats (16-byte aligned rows)
+constexpr int kPadKC = 2;  // [o][k] rows: 16 + 2 floats (8-byte aligned rows)
+constexpr int kRowKC = kBK + kPadKC;
 
-// Per-thread loader of one operand tile.  Shared layout for both operands:
-// [k][o] rows of BO + kPad floats.
-//   MC (outer-contiguous source, element (o, k) at X[o + k*ld]): VEC-float
-//     chunks along o; the thread's o is fixed, its k advances by NT / CPR.
-//   KC (k-contiguous source, element (o, k) at X[k + o*ld]): transposed by
-//     4-byte copies, consecutive threads walk k (contiguous global
-//     addresses); the thread's k is fixed, its o advances by NT / kBK.
-// The thread's global pointer is computed once and advanced per k-tile.
+template <int BO, bool KC>
+struct FLayout {
+  static constexpr int ELEMS = KC ? BO * kRowKC : kBK * (BO + kPadMC);
+};
+
+// Per-thread loader.  MC: (o, k) at X[o + k*ld], chunks of VEC floats along
+// o into [k][o]; KC: (o, k) at X[k + o*ld], chunks of VEC floats along k into
+// [o][k].  The thread's chunk column is fixed, its row advances by STEP.
 template <int BO, int NT, int VEC, bool KC>
 struct FLoader {
-  static constexpr int RS = BO + kPad;
-  static constexpr int CPR = KC ? kBK : BO / VEC;  // copies per shared row (KC: per o)
-  static constexpr int IT = kBK * BO / VEC / NT;
-  static constexpr int STEP = NT / CPR;            // MC: k rows, KC: o rows per iteration
-  static_assert(!KC || VEC == 1, "KC copies are 4-byte transposes");
-  static_assert(NT % CPR == 0 && (kBK * BO / VEC) % NT == 0, "loader trip count");
+  static constexpr int WIDTH = KC ? kBK : BO;  // source run length per row
+  static constexpr int CPR = WIDTH / VEC;
+  static constexpr int ROWS = KC ? BO : kBK;
+  static constexpr int IT = CPR * ROWS / NT;
+  static constexpr int STEP = NT / CPR;
+  static_assert(NT % CPR == 0 && (CPR * ROWS) % NT == 0, "loader trip count");
 
   const float* base;
   const float* p0;
   i64 ld, step;
-  int k_first, o_first;
+  int row0, col;
   int o_lim, k_lim, fix_bytes;
 
   __device__ void init(const float* X, i64 ld_, i64 o0, i64 O, i64 K) {
     ld = ld_;
-    const int q = threadIdx.x;
-    if (KC) {
-      k_first = q % kBK;
-      o_first = q / kBK;
-    } else {
-      o_first = (q % CPR) * VEC;
-      k_first = q / CPR;
-    }
+    row0 = threadIdx.x / CPR;
+    col = (threadIdx.x % CPR) * VEC;
     o_lim = static_cast<int>(O - o0 < (1 << 30) ? O - o0 : (1 << 30));
     k_lim = static_cast<int>(K < (1 << 30) ? K : (1 << 30));
     base = KC ? X + o0 * ld : X + o0;
-    p0 = KC ? base + static_cast<i64>(o_first) * ld + k_first : base + o_first + static_cast<i64>(k_first) * ld;
+    p0 = base + static_cast<i64>(row0) * ld + col;  // (row, col) at base + row*ld + col
     step = static_cast<i64>(STEP) * ld;
-    const int rem = o_lim - o_first;
+    const int rem = o_lim - col;
     fix_bytes = rem >= VEC ? VEC * 4 : (rem > 0 ? rem * 4 : 0);
   }
 
@@ -65,15 +67,48 @@ struct FLoader {
     const float* tb = p0 + (KC ? static_cast<i64>(k0) : static_cast<i64>(k0) * ld);
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      const int o = o_first + (KC ? it * STEP : 0);
-      const int k = k_first + (KC ? 0 : it * STEP);
+      const int row = row0 + it * STEP;
       int bytes;
-      if (KC) bytes = (o < o_lim && k0 + k < k_lim) ? 4 : 0;
-      else bytes = (k0 + k < k_lim) ? fix_bytes : 0;
+      if (KC) {
+        const int rem = k_lim - (k0 + col);
+        bytes = row < o_lim ? (rem >= VEC ? VEC * 4 : (rem > 0 ? rem * 4 : 0)) : 0;
+      } else {
+        bytes = (k0 + row < k_lim) ? fix_bytes : 0;
+      }
       const float* g = bytes ? tb + it * step : base;
-      float* dst = s + k * RS + o;
+      float* dst = KC ? s + row * kRowKC + col : s + row * (BO + kPadMC) + col;
       if constexpr (VEC == 4) cp_async16(dst, g, bytes);
+      else if constexpr (VEC == 2) cp_async8(dst, g, bytes);
       else cp_async4(dst, g, bytes);
+    }
+  }
+};
+
+// The thread's 8 outer indices of an operand and how to read them.
+template <int BO, bool KC>
+struct FFrag {
+  // index j (0..7) of thread t (0..15 along this operand)
+  __device__ static int outer(int t, int j) {
+    return KC ? t + 16 * j : (j < 4 ? 4 * t + j : BO / 2 + 4 * t + j - 4);
+  }
+  // values for k-steps k and k+1: v[0][j] (k), v[1][j] (k+1)
+  __device__ static void read(const float* s, int t, int k, float (&v)[2][8]) {
+    if constexpr (KC) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2 x = *reinterpret_cast<const float2*>(s + (t + 16 * j) * kRowKC + k);
+        v[0][j] = x.x;
+        v[1][j] = x.y;
+      }
+    } else {
+      constexpr int RS = BO + kPadMC;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 a = *reinterpret_cast<const float4*>(s + (k + h) * RS + 4 * t);
+        const float4 b = *reinterpret_cast<const float4*>(s + (k + h) * RS + BO / 2 + 4 * t);
+        v[h][0] = a.x; v[h][1] = a.y; v[h][2] = a.z; v[h][3] = a.w;
+        v[h][4] = b.x; v[h][5] = b.y; v[h][6] = b.z; v[h][7] = b.w;
+      }
     }
   }
 };
@@ -82,24 +117,22 @@ template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB>
 __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
     sgemm_ffma_kernel(const GemmParams<float> p) {
   constexpr int TX = BN / 8, TY = BM / 8, NT = TX * TY;
-  constexpr int RSA = BM + kPad, RSB = BN + kPad;
+  static_assert(TX == 16 && TY == 16, "16 x 16 thread grid");
+  constexpr bool A_KC = TA, B_KC = !TB;  // k-contiguous sources
+  constexpr int A_EL = FLayout<BM, A_KC>::ELEMS, B_EL = FLayout<BN, B_KC>::ELEMS;
   extern __shared__ __align__(128) float fsmem[];
   float* sA = fsmem;
-  float* sB = fsmem + STAGES * kBK * RSA;
+  float* sB = fsmem + STAGES * A_EL;
 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const i64 m0 = static_cast<i64>(blockIdx.x) * BM;
   const i64 n0 = static_cast<i64>(blockIdx.y) * BN;
   const i64 KT = ceil_div(p.K, kBK);
 
-  FLoader<BM, NT, TA ? 1 : VA, TA> la;
-  FLoader<BN, NT, TB ? VB : 1, !TB> lb;
+  FLoader<BM, NT, VA, A_KC> la;
+  FLoader<BN, NT, VB, B_KC> lb;
   la.init(p.A, p.lda, m0, p.M, p.K);
   lb.init(p.B, p.ldb, n0, p.N, p.K);
-  auto load_stage = [&](int stage, i64 kt) {
-    la.load(sA + stage * kBK * RSA, kt);
-    lb.load(sB + stage * kBK * RSB, kt);
-  };
 
   float acc[8][8];
 #pragma unroll
@@ -109,7 +142,10 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(s, s);
+    if (s < KT) {
+      la.load(sA + s * A_EL, s);
+      lb.load(sB + s * B_EL, s);
+    }
     cp_async_commit();
   }
   for (i64 kt = 0; kt < KT; ++kt) {
@@ -117,24 +153,27 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
     __syncthreads();
     {
       const i64 nk = kt + STAGES - 1;
-      if (nk < KT) load_stage(static_cast<int>(nk % STAGES), nk);
+      if (nk < KT) {
+        const int ws = static_cast<int>(nk % STAGES);
+        la.load(sA + ws * A_EL, nk);
+        lb.load(sB + ws * B_EL, nk);
+      }
       cp_async_commit();
     }
     const int st = static_cast<int>(kt % STAGES);
-    const float* a_s = sA + st * kBK * RSA;
-    const float* b_s = sB + st * kBK * RSB;
+    const float* a_s = sA + st * A_EL;
+    const float* b_s = sB + st * B_EL;
 #pragma unroll
-    for (int k = 0; k < kBK; ++k) {
-      const float4 a0 = *reinterpret_cast<const float4*>(a_s + k * RSA + ty * 4);
-      const float4 a1 = *reinterpret_cast<const float4*>(a_s + k * RSA + BM / 2 + ty * 4);
-      const float4 b0 = *reinterpret_cast<const float4*>(b_s + k * RSB + tx * 4);
-      const float4 b1 = *reinterpret_cast<const float4*>(b_s + k * RSB + BN / 2 + tx * 4);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    for (int k = 0; k < kBK; k += 2) {
+      float av[2][8], bv[2][8];
+      FFrag<BM, A_KC>::read(a_s, ty, k, av);
+      FFrag<BN, B_KC>::read(b_s, tx, k, bv);
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[h][i], bv[h][j], acc[i][j]);
     }
   }
   cp_async_wait<0>();
@@ -142,11 +181,11 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
   const bool beta_zero = p.beta == 0.f;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const i64 n = n0 + (j < 4 ? tx * 4 + j : BN / 2 + tx * 4 + j - 4);
+    const i64 n = n0 + FFrag<BN, B_KC>::outer(tx, j);
     if (n >= p.N) continue;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const i64 m = m0 + (i < 4 ? ty * 4 + i : BM / 2 + ty * 4 + i - 4);
+      const i64 m = m0 + FFrag<BM, A_KC>::outer(ty, i);
       if (m < p.M) {
         float* c = p.C + m + n * p.ldc;
         *c = beta_zero ? p.alpha * acc[i][j] : fmaf(p.alpha, acc[i][j], p.beta * *c);
@@ -158,28 +197,32 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
 template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB>
 void launch_cfg(const GemmParams<float>& p, cudaStream_t s) {
   auto kern = sgemm_ffma_kernel<BM, BN, STAGES, TA, TB, VA, VB>;
-  constexpr int smem = STAGES * kBK * (BM + BN + 2 * kPad) * static_cast<int>(sizeof(float));
+  constexpr int smem =
+      STAGES * (FLayout<BM, TA>::ELEMS + FLayout<BN, !TB>::ELEMS) * static_cast<int>(sizeof(float));
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
   kern<<<grid, (BM / 8) * (BN / 8), smem, s>>>(p);
   ++launch_counter();
 }
 
-bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
+bool aligned(const void* ptr, unsigned b) { return (reinterpret_cast<uintptr_t>(ptr) & (b - 1)) == 0; }
 
+// Copy width per operand: outer-contiguous sources use 16-byte chunks when
+// 16-byte aligned (else 4-byte); k-contiguous sources use 8-byte chunks when
+// 8-byte aligned (else 4-byte).
 template <int BM, int BN, int STAGES>
 void dispatch(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
-  // The vector width only applies to outer-contiguous operands (A when !ta,
-  // B when tb); it needs 16-byte aligned columns.
-  const bool va = !ta && aligned16(p.A) && p.lda % 4 == 0;
-  const bool vb = tb && aligned16(p.B) && p.ldb % 4 == 0;
-#define RECTRI_CFG(TA_, TB_)                                                   \
-  if (ta == TA_ && tb == TB_) {                                                \
-    if (va && vb) launch_cfg<BM, BN, STAGES, TA_, TB_, 4, 4>(p, s);            \
-    else if (va) launch_cfg<BM, BN, STAGES, TA_, TB_, 4, 1>(p, s);             \
-    else if (vb) launch_cfg<BM, BN, STAGES, TA_, TB_, 1, 4>(p, s);             \
-    else launch_cfg<BM, BN, STAGES, TA_, TB_, 1, 1>(p, s);                     \
-    return;                                                                    \
+  const bool a_kc = ta, b_kc = !tb;
+  const bool va = a_kc ? (aligned(p.A, 8) && p.lda % 2 == 0) : (aligned(p.A, 16) && p.lda % 4 == 0);
+  const bool vb = b_kc ? (aligned(p.B, 8) && p.ldb % 2 == 0) : (aligned(p.B, 16) && p.ldb % 4 == 0);
+#define RECTRI_CFG(TA_, TB_)                                                              \
+  if (ta == TA_ && tb == TB_) {                                                           \
+    constexpr int WA = TA_ ? 2 : 4, WB = TB_ ? 4 : 2;                                     \
+    if (va && vb) launch_cfg<BM, BN, STAGES, TA_, TB_, WA, WB>(p, s);                     \
+    else if (va) launch_cfg<BM, BN, STAGES, TA_, TB_, WA, 1>(p, s);                       \
+    else if (vb) launch_cfg<BM, BN, STAGES, TA_, TB_, 1, WB>(p, s);                       \
+    else launch_cfg<BM, BN, STAGES, TA_, TB_, 1, 1>(p, s);                                \
+    return;                                                                               \
   }
   RECTRI_CFG(false, false)
   RECTRI_CFG(true, false)
@@ -192,10 +235,7 @@ void dispatch(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
 
 void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
-  if (p.M >= 128 && p.N >= 128) dispatch<128, 128, 3>(p, ta, tb, s);
-  else if (p.N >= 128) dispatch<64, 128, 3>(p, ta, tb, s);
-  else if (p.M >= 128) dispatch<128, 64, 3>(p, ta, tb, s);
-  else dispatch<64, 64, 3>(p, ta, tb, s);
+  dispatch<128, 128, 3>(p, ta, tb, s);
 }
 
 }  // namespace rectri_cu

@@ -152,9 +152,33 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm0 = (warp % WARPS_M) * WM, wn0 = (warp / WARPS_M) * WN;
-  const i64 m0 = static_cast<i64>(blockIdx.x) * BM;
-  const i64 n0 = static_cast<i64>(blockIdx.y) * BN;
+  // Grouped rasterization of a 1-D grid: consecutive CTAs walk kGroup
+  // M-tiles down one N column, then the next column, so the CTAs resident at
+  // any time share A row-panels and B column-panels in L2 (an M-fastest grid
+  // re-streamed all of A from DRAM for every N column).
+  constexpr int kGroup = 16;
+  const int tiles_m = static_cast<int>(ceil_div(p.M, BM));
+  const int tiles_n = static_cast<int>(ceil_div(p.N, BN));
+  const int lin = static_cast<int>(blockIdx.x);
+  const int per_group = kGroup * tiles_n;
+  const int grp = lin / per_group, in_grp = lin - grp * per_group;
+  const int gm0 = grp * kGroup;
+  const int gsize = min(kGroup, tiles_m - gm0);
+  const int tm = gm0 + in_grp % gsize, tn = in_grp / gsize;
+  const i64 m0 = static_cast<i64>(tm) * BM;
+  const i64 n0 = static_cast<i64>(tn) * BN;
   const i64 KT = ceil_div(p.K, kBK);
+
+  // Warm L2 with this CTA's C tile (read by the epilogue) while the
+  // mainloop runs: one prefetch per 128-byte line of each column.
+  if (p.beta != 0.0) {
+    constexpr int LINES = BM * 8 / 128;  // lines per column
+    for (int q = threadIdx.x; q < BN * LINES; q += NT) {
+      const i64 n = n0 + q / LINES, m = m0 + (q % LINES) * 16;
+      if (n < p.N && m < p.M)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p.C + m + n * p.ldc));
+    }
+  }
 
   TileLoader<BM, BK, NT, VEC, TA, MCMODE> la;
   TileLoader<BN, BK, NT, VEC, !TB, MCMODE> lb;
@@ -284,7 +308,7 @@ struct Config {
     constexpr int pad = MCMODE == 1 ? 4 : 0;
     constexpr int smem = STAGES * (BM + BN + 2 * pad) * BK * static_cast<int>(sizeof(double));
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
+    const unsigned grid = static_cast<unsigned>(ceil_div(p.M, BM) * ceil_div(p.N, BN));
     kern<<<grid, WARPS_M * WARPS_N * 32, smem, s>>>(p);
     ++launch_counter();
   }
@@ -324,7 +348,9 @@ using DgemmRun = void (*)(const GemmParams<double>&, bool, bool, bool, cudaStrea
   X(13, 128, 64, 16, 2, 2, 4)            \
   X(14, 64, 64, 16, 2, 1, 4)             \
   X(15, 64, 64, 16, 2, 2, 4)             \
-  X(16, 64, 64, 16, 2, 2, 4)
+  X(16, 64, 64, 16, 2, 2, 4)             \
+  X(17, 64, 64, 16, 4, 2, 4)             \
+  X(18, 64, 64, 16, 2, 4, 4)
 #define RECTRI_DECL(ID, BM, BN, BK, WM, WN, ST) \
   void dgemm_cfg##ID(const GemmParams<double>&, bool, bool, bool, cudaStream_t);
 RECTRI_DGEMM_CONFIGS(RECTRI_DECL)
