@@ -37,9 +37,11 @@ int choose(const GemmParams<double>& p) {
   // eligible when K % 32 == 0, where both produce identical bits.
   const bool bk32 = f == 2 || f == 3 || f == 7 || f == 8 || f == 9;
   if (f >= 0 && f < kNumCfg && (p.K % 32 == 0 || !bk32)) return f;
-  // 64x64 CTAs (4 warps, 3 per SM): measured best at every level shape of
-  // the recursion on B200 (profiles/r01_gemm_cfg_sweep.txt).
-  return 6;
+  // 64x64 CTAs: 4 warps (3 CTAs per SM) for the large levels, 8 warps (2 per
+  // SM) when K <= 512 where more resident warps hide the short mainloop's
+  // prologue/epilogue latency (profiles/r01_gemm_cfg_sweep.txt).  Both use
+  // 16-deep k-tiles: identical per-element arithmetic.
+  return p.K <= 512 ? 17 : 6;
 }
 
 }  // namespace
