@@ -134,11 +134,23 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
   la.init(p.A, p.lda, m0, p.M, p.K);
   lb.init(p.B, p.ldb, n0, p.N, p.K);
 
+  // A outer-contiguous (op N): the thread's m values come in adjacent pairs
+  // (LDS.128), so accumulators are packed as m-pairs and updated with the
+  // packed FFMA2 (fma.rn.f32x2, B value broadcast as a scalar operand): two
+  // independent round-to-nearest FMAs per instruction, bitwise the same as
+  // two fmaf, at half the issue slots and register-bank reads per FMA.
+  // A k-contiguous (op T): scalar FFMA.
+  constexpr bool kPacked = !A_KC;
   float acc[8][8];
+  unsigned long long acc2[4][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc2[i][j] = 0ull;
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -169,14 +181,36 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
       FFrag<BM, A_KC>::read(a_s, ty, k, av);
       FFrag<BN, B_KC>::read(b_s, tx, k, bv);
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < 2; ++h) {
+        if constexpr (kPacked) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+          for (int ip = 0; ip < 4; ++ip) {
+            unsigned long long ap;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(ap) : "f"(av[h][2 * ip]), "f"(av[h][2 * ip + 1]));
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[h][i], bv[h][j], acc[i][j]);
+            for (int j = 0; j < 8; ++j) {
+              unsigned long long bb;
+              asm("mov.b64 %0, {%1, %1};" : "=l"(bb) : "f"(bv[h][j]));
+              asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[ip][j]) : "l"(ap), "l"(bb));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[h][i], bv[h][j], acc[i][j]);
+        }
+      }
     }
   }
   cp_async_wait<0>();
+  if constexpr (kPacked) {
+#pragma unroll
+    for (int ip = 0; ip < 4; ++ip)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[2 * ip][j]), "=f"(acc[2 * ip + 1][j]) : "l"(acc2[ip][j]));
+  }
 
   const bool beta_zero = p.beta == 0.f;
 #pragma unroll

@@ -26,8 +26,10 @@ if kind in ("trsm", "trmm"):
     rc.fill_uniform(B.view(), seed=2)
     fn = rc.rec_trsm if kind == "trsm" else rc.rec_trmm
     fn(TriangularSpec(), A.cview(), B.view(), Threshold(t), be)
-elif kind in ("gemm", "gemmtn"):
+elif kind in ("gemm", "gemmtn", "sgemm"):
     M, N, K = args
+    if kind == "sgemm":
+        f64 = torch.float32
     ta = Trans.Trans if kind == "gemmtn" else Trans.NoTrans
     A = MatrixBuffer(K, M, f64, "cuda") if kind == "gemmtn" else MatrixBuffer(M, K, f64, "cuda")
     B = MatrixBuffer(K, N, f64, "cuda")
