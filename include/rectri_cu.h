@@ -185,6 +185,16 @@ double rectri_cu_probe_peak(int32_t kind);
  * 3 = pivot scan: device milliseconds, launches and algorithmic flops
  * (GEMM 2MNK, leaf nb^2 * rhs), then clears the record. */
 void rectri_cu_profile_enable(int32_t on);
+
+/* Benchmark-harness helpers (bench CLI parity): the reference's input
+ * generator (src/bench.cpp:32-61) and residual-gate column sample
+ * (:109-117), evaluated with libstdc++ <random> -> bit-identical streams.
+ * Host buffers, column-major (A n x n, B brows x bcols). */
+void rectri_cu_bench_inputs_f64(double* a, double* b, int64_t n, int64_t brows, int64_t bcols,
+                                int32_t is_trsm, int32_t uplo, int32_t diag, uint64_t seed);
+void rectri_cu_bench_inputs_f32(float* a, float* b, int64_t n, int64_t brows, int64_t bcols,
+                                int32_t is_trsm, int32_t uplo, int32_t diag, uint64_t seed);
+int32_t rectri_cu_gate_columns(uint64_t seed, int64_t cols, int64_t out[8]);
 int rectri_cu_profile_read(double ms[4], int64_t launches[4], double flops[4]);
 
 #ifdef __cplusplus

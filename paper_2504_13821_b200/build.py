@@ -21,7 +21,7 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "lib" / "obj"
 LIB = PKG / "lib" / "librectri_cu.so"
 SOURCES = ["gemm_f64.cu", *[f"gemm_f64_cfg{i}.cu" for i in range(19)], "gemm_f32.cu", "leaf.cu", "aux.cu",
-           "driver.cu"]
+           "driver.cu", "bench_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
     "-O3",
@@ -67,7 +67,7 @@ def build(verbose: bool = False) -> Path:
     objs = []
     for name in SOURCES:
         src = CSRC / name
-        obj = OBJ / (name.replace(".cu", ".o"))
+        obj = OBJ / (name.rsplit(".", 1)[0] + ".o")
         objs.append(obj)
         if _stale(obj, [src, *headers]):
             jobs.append((src, obj))

@@ -43,7 +43,9 @@ struct LeafParams {
   int unit;
   int trsm;  // 1: solve, 0: multiply
   T alpha;
-  int debug_skip = 0;  // timing experiments only (RECTRI_CU_LEAF_DEBUG): 1 no diag part, 2 no GEMM part
+  // Experiments only (RECTRI_CU_LEAF_DEBUG): 1 no diagonal part, 2 no GEMM
+  // part (timing), 3 planted missing barrier (racecheck negative test).
+  int debug_skip = 0;
 };
 
 constexpr int kLeafMax = 256;

@@ -386,7 +386,10 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(const LeafParams<T> p) {
     const T* ld = ring + (s % kRing) * LeafSmem<T>::blk;
     if (p.trsm) gp.store(panel, r0, neg);
     else gp.store(ys, 0, false);
-    __syncthreads();
+    // debug_skip == 3 plants a race (missing barrier) for the racecheck
+    // negative test (tests/test_gpu_sanitizer.py), cf. the reference's
+    // build_trsm_program_missing_barrier (workgroup.cpp:333-349).
+    if (p.debug_skip != 3) __syncthreads();
     if (p.debug_skip == 1) continue;
     T v[4];
     if (p.trsm) {

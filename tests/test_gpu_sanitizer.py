@@ -1,0 +1,39 @@
+"""Race / sync / memory checking of the real kernels with compute-sanitizer
+(the role of the reference's workgroup simulator and its planted-race test,
+workgroup.cpp:138-177, 333-349; test_workgroup.cpp:144-176)."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+SAN = "/usr/local/cuda/bin/compute-sanitizer"
+
+
+def _san(tool, args, env_extra=None):
+    env = dict(os.environ)
+    env.update(env_extra or {})
+    cmd = [SAN, "--tool", tool, "--kernel-name", "kns=rectri_cu", "--print-limit", "5",
+           sys.executable, str(ROOT / "tools" / "prof_run.py"), *args]
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+
+
+@pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
+@pytest.mark.parametrize("args", [["leaf", "100", "70"], ["trmmleaf", "100", "70"], ["gemm", "130", "70", "50"],
+                                  ["trsm", "300", "40", "64"]])
+def test_kernels_clean(cuda, tool, args):
+    r = _san(tool, args)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-3000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-3000:]
+    if tool == "racecheck":
+        assert "RACECHECK SUMMARY: 0 hazards" in out or "0 hazards displayed" in out, out[-3000:]
+
+
+def test_planted_race_is_detected(cuda):
+    r = _san("racecheck", ["leaf", "100", "70"], {"RECTRI_CU_LEAF_DEBUG": "3"})
+    out = r.stdout + r.stderr
+    assert "hazard" in out.lower() and "0 hazards" not in out, out[-3000:]

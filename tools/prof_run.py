@@ -37,13 +37,14 @@ elif kind in ("gemm", "gemmtn", "sgemm"):
     for i, x in enumerate((A, B, C)):
         rc.fill_uniform(x.view(), seed=i)
     rc.gemm(-1.0, ta, A.cview(), Trans.NoTrans, B.cview(), 1.0, C.view(), be)
-elif kind == "leaf":
+elif kind in ("leaf", "trmmleaf"):
     nb, m = args
     A = MatrixBuffer(nb, nb, f64, "cuda")
     rc.fill_uniform(A.view(), seed=1)
     rc.make_dominant(A.view())
     B = MatrixBuffer(nb, m, f64, "cuda")
     rc.fill_uniform(B.view(), seed=2)
-    rc.trsm_base(TriangularSpec(), A.cview(), B.view(), nb, be)
+    fn = rc.trsm_base if kind == "leaf" else rc.trmm_base
+    fn(TriangularSpec(), A.cview(), B.view(), nb, be)
 torch.cuda.synchronize()
 print("done", kind, args)
