@@ -20,7 +20,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "lib" / "obj"
 LIB = PKG / "lib" / "librectri_cu.so"
-SOURCES = ["gemm_f64.cu", *[f"gemm_f64_cfg{i}.cu" for i in range(19)], "gemm_f32.cu", "leaf.cu", "aux.cu",
+SOURCES = ["gemm_f64.cu", *[f"gemm_f64_cfg{i}.cu" for i in range(19)], "gemm_f64_tma.cu",
+           *[f"gemm_f64_tma_cfg{i}.cu" for i in range(7)], "gemm_f32.cu", "leaf.cu", "aux.cu",
            "driver.cu", "bench_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [

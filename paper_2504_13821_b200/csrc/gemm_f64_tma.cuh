@@ -1,0 +1,279 @@
+// gemm_f64_tma.cuh -- fp64 DMMA GEMM update fed by TMA + mbarrier pipelines.
+//
+// Same contract and the same per-element arithmetic as gemm_f64_kernel.cuh
+// (the cp.async kernel, kept for operands TMA cannot describe): it replaces
+// the reference's blocked CPU GEMM (src/gemm.cpp:155-216) for the
+// recursion's off-diagonal updates (recursion.cpp:134-143).
+//
+// Data movement: one elected thread (a dedicated producer warp, or lane 0 of
+// warp 0) issues cp.async.bulk.tensor (TMA) copies of each 16-deep k-tile of
+// op(A) and op(B) into a STAGES-deep shared ring; TMA zero-fills every
+// out-of-range element (exact 0, never a multiply-by-mask).  Each stage has a
+// `full` mbarrier (armed with the byte count, completed by the TMA) and an
+// `empty` mbarrier (one arrival per consumer warp once its last fragment read
+// of the stage is done).  No __syncthreads in the mainloop, no per-thread
+// address arithmetic for global loads.
+//
+// Shared layouts (8-byte elements):
+//   outer-contiguous operand (A NoTrans / B Trans): plain 2D box {BO, 16},
+//     element (o, k) at k*BO + o.  Fragment reads are 16-byte pairs
+//     (ld.shared.v2.f64): the mma row/column permutation below gives each
+//     thread two adjacent outer indices, so a warp reads 4 full 128-byte rows
+//     -- 4 wavefronts for 512 bytes, the minimum.
+//   k-contiguous operand (A Trans / B NoTrans): 2D box {16, BO} with the
+//     128-byte TMA swizzle, element (o, k) at o*16 + 2*((k/2) ^ (o%8)) + k%2;
+//     8-byte fragment reads are conflict-free (2 wavefronts per 256 bytes).
+//
+// Permutations (free: they only relabel which output row/column an mma
+// lane-slot holds, never the k order): for outer-contiguous A, mma row r of
+// 16-row tile i is m = 16i + 2(r%8) + r/8; for outer-contiguous B, the two
+// 8-column mma tiles 2q, 2q+1 interleave: column c of tile j is
+// n = 16q + 2c + (j%2).
+//
+// Determinism: each output element is accumulated over k in 16-wide k-tiles
+// of four m16n8k4 steps from a zero accumulator, then C = fma(alpha, acc,
+// beta*C) -- exactly the cp.async kernel's sequence, so the two kernels (and
+// every tile shape) produce identical bits.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace rectri_cu {
+namespace dgemm_tma {
+
+constexpr int kBK = 16;
+
+__device__ __forceinline__ void dmma1684(double (&c)[4], double a0, double a1, double b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void lds64(double& x, uint32_t a) {
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(x) : "r"(a));
+}
+__device__ __forceinline__ void lds128(double& x, double& y, uint32_t a) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(a));
+}
+
+// STAGES-deep ring; CONSUMER warps WARPS_M x WARPS_N each own WM x WN;
+// PRODUCER: a dedicated 32-thread producer warp (else lane 0 of warp 0).
+// MC_A: A tile outer(m)-contiguous (op(A) = A); MC_B: B tile outer(n)-contiguous
+// (op(B) = B^T).
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B>
+__global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32, 1)
+    dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapB, const GemmParams<double> p) {
+  constexpr int NCW = WARPS_M * WARPS_N;  // consumer warps
+  constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
+  constexpr int TM = WM / 16, TN = WN / 8;
+  static_assert(WM % 16 == 0 && WN % 16 == 0, "warp tile");
+  constexpr uint32_t A_BYTES = BM * kBK * 8, B_BYTES = BN * kBK * 8;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for the 128-byte swizzle atoms.
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  const uint32_t bars = sbase + STAGES * STAGE_BYTES;  // full[s] at +8s, empty[s] at +8(STAGES+s)
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
+  auto stage_a = [&](int s) { return sbase + s * STAGE_BYTES; };
+  auto stage_b = [&](int s) { return sbase + s * STAGE_BYTES + A_BYTES; };
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  // Grouped rasterization (as the cp.async kernel): consecutive CTAs walk 16
+  // M-tiles down one N column so resident CTAs share panels in L2.
+  constexpr int kGroup = 16;
+  const int tiles_m = static_cast<int>(ceil_div(p.M, BM));
+  const int tiles_n = static_cast<int>(ceil_div(p.N, BN));
+  const int lin = static_cast<int>(blockIdx.x);
+  const int per_group = kGroup * tiles_n;
+  const int grp = lin / per_group, in_grp = lin - grp * per_group;
+  const int gm0 = grp * kGroup;
+  const int gsize = min(kGroup, tiles_m - gm0);
+  const int tm = gm0 + in_grp % gsize, tn = in_grp / gsize;
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int KT = static_cast<int>(ceil_div(p.K, kBK));
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int kf) {  // one elected thread: fill stage kf % STAGES with k-tile kf
+    const int s = kf % STAGES;
+    mbar_expect_tx(full_bar(s), STAGE_BYTES);
+    // outer-contiguous: dims {O, K}, coords {o0, k0}; k-contiguous: {K, O}, {k0, o0}
+    if (MC_A) tma_load_2d(stage_a(s), &mapA, m0, kf * kBK, full_bar(s));
+    else tma_load_2d(stage_a(s), &mapA, kf * kBK, m0, full_bar(s));
+    if (MC_B) tma_load_2d(stage_b(s), &mapB, n0, kf * kBK, full_bar(s));
+    else tma_load_2d(stage_b(s), &mapB, kf * kBK, n0, full_bar(s));
+  };
+
+  if (PRODUCER && warp == NCW) {
+    if (lane == 0) {
+      for (int kf = 0; kf < KT; ++kf) {
+        if (kf >= STAGES) mbar_wait(empty_bar(kf % STAGES), ((kf / STAGES) + 1) & 1);
+        issue(kf);
+      }
+    }
+    return;
+  }
+  constexpr int kAhead = PRODUCER ? 0 : STAGES - 1;  // inline producer keeps STAGES-1 tiles in flight
+  if (!PRODUCER && threadIdx.x == 0) {
+    for (int kf = 0; kf < kAhead && kf < KT; ++kf) issue(kf);
+  }
+
+  // Consumers.
+  const int g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp % WARPS_M) * WM, wn0 = (warp / WARPS_M) * WN;
+  // Byte offsets within a stage's A / B tile for k-step 0 (k-steps add a
+  // constant for outer-contiguous tiles; k-contiguous tiles use xo[kk]).
+  // k-contiguous swizzled element (o, k): o*128 + (((k>>1) ^ (o&7)) << 4) + (k&1)*8,
+  // with o&7 == g for every fragment row/column this thread reads.
+  uint32_t xo[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+    xo[kk] = static_cast<uint32_t>(((((4 * kk + t) >> 1) ^ g) << 4) + (t & 1) * 8);
+  const uint32_t a_mc = static_cast<uint32_t>((t * BM + wm0 + 2 * g) * 8);
+  const uint32_t a_kc = static_cast<uint32_t>((wm0 + g) * 128);
+  const uint32_t b_mc = static_cast<uint32_t>((t * BN + wn0 + 2 * g) * 8);
+  const uint32_t b_kc = static_cast<uint32_t>((wn0 + g) * 128);
+
+  double af[2][TM][2], bf[2][TN];
+  auto load_frags = [&](int buf, int s, int kk) {
+    const uint32_t as = stage_a(s), bs = stage_b(s);
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      if (MC_A) {
+        lds128(af[buf][i][0], af[buf][i][1], as + a_mc + (kk * 4 * BM + 16 * i) * 8);
+      } else {
+        lds64(af[buf][i][0], as + a_kc + xo[kk] + (16 * i) * 128);
+        lds64(af[buf][i][1], as + a_kc + xo[kk] + (16 * i + 8) * 128);
+      }
+    }
+    if (MC_B) {
+#pragma unroll
+      for (int q = 0; q < TN / 2; ++q)
+        lds128(bf[buf][2 * q], bf[buf][2 * q + 1], bs + b_mc + (kk * 4 * BN + 16 * q) * 8);
+    } else {
+#pragma unroll
+      for (int j = 0; j < TN; ++j) lds64(bf[buf][j], bs + b_kc + xo[kk] + (8 * j) * 128);
+    }
+  };
+
+  double acc[TM][TN][4];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+  if (KT > 0) {
+    mbar_wait(full_bar(0), 0);
+    load_frags(0, 0, 0);
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    if (!PRODUCER && threadIdx.x == 0) {
+      const int kf = kt + kAhead;
+      if (kf < KT) {
+        if (kf >= STAGES) mbar_wait(empty_bar(kf % STAGES), ((kf / STAGES) + 1) & 1);
+        issue(kf);
+      }
+    }
+    const int s = kt % STAGES;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int cb = kk & 1, nb = cb ^ 1;
+      if (kk < 3) {
+        load_frags(nb, s, kk + 1);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_bar(s));  // this warp is done reading stage s
+        if (kt + 1 < KT) {
+          const int s1 = (kt + 1) % STAGES;
+          mbar_wait(full_bar(s1), ((kt + 1) / STAGES) & 1);
+          load_frags(nb, s1, 0);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma1684(acc[i][j], af[cb][i][0], af[cb][i][1], bf[cb][j]);
+    }
+  }
+
+  // Epilogue: C = fma(alpha, acc, beta*C) (beta == 0 never reads C).
+  const bool beta_zero = p.beta == 0.0;
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const i64 m = m0 + wm0 + 16 * i + (MC_A ? 2 * g + h : 8 * h + g);
+      if (m >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 2 * t + e;
+          const i64 n = n0 + wn0 + (MC_B ? 16 * (j >> 1) + 2 * c + (j & 1) : 8 * j + c);
+          if (n < p.N) {
+            double* cp = p.C + m + n * p.ldc;
+            const double v = acc[i][j][2 * h + e];
+            *cp = beta_zero ? p.alpha * v : fma(p.alpha, v, p.beta * *cp);
+          }
+        }
+    }
+}
+
+}  // namespace dgemm_tma
+
+// Returns false (nothing launched) when TMA cannot describe the operands
+// (unaligned base / odd leading dimension / index range beyond int32).
+bool launch_gemm_f64_tma(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s, int cfg);
+
+}  // namespace rectri_cu
