@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -365,7 +366,9 @@ void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaSt
 // ---------------------------------------------------------------------------
 // Per-device resources: capture stream and a staging pool for host views.
 struct DeviceRes {
+  static constexpr int kAux = 3;  // extra streams of the right-hand-side panel split
   cudaStream_t capture = nullptr;
+  cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr};
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the staged path
   static constexpr int kSlots = 3;            // 0: A, 1..2: B panels
   void* stage[kSlots] = {nullptr, nullptr, nullptr};
@@ -381,8 +384,19 @@ DeviceRes& device_res(int dev) {
     cuda_check(cudaStreamCreateWithFlags(&r.capture, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&r.h2d, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking), "stream");
+    for (auto& a : r.aux) cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
   }
   return r;
+}
+
+// Streams the right-hand sides are split over (RECTRI_CU_STREAMS, default 2;
+// panels narrower than 2048 right-hand sides are not split).
+int panel_streams(i64 rhs) {
+  const char* e = getenv("RECTRI_CU_STREAMS");
+  int p = e ? atoi(e) : 2;
+  if (p > DeviceRes::kAux + 1) p = DeviceRes::kAux + 1;
+  while (p > 1 && rhs / p < 2048) --p;
+  return p < 1 ? 1 : p;
 }
 
 void* staging(DeviceRes& r, int slot, size_t bytes) {
@@ -480,7 +494,13 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
   Spec eff = spec;
   i64& counter = launch_counter();
   const i64 before = counter;
-  if (capture) cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+  if (capture) {
+    // per-stream leaf scratch must exist before capture (no allocation inside)
+    DeviceRes& res = device_res(dev);  // the capture path holds g_mu
+    leaf_scratch_reserve(s);
+    for (cudaStream_t a : res.aux) leaf_scratch_reserve(a);
+    cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+  }
   if (op == kTrsm) {
     if (spec.alpha != 1.0) {
       ProfScope prof(2, 0.0, s);
@@ -493,7 +513,52 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
     K<T>::scan(A.p, A.ld, A.rows, g->d_flags, s);
     cudaMemcpyAsync(g->h_flags, g->d_flags, static_cast<size_t>(A.rows), cudaMemcpyDeviceToHost, s);
   }
-  Recursion<T>(op, threshold, s, &g->events, &g->leaves).run(eff, A, B, 0);
+  const bool left = spec.side == RECTRI_CU_LEFT;
+  const i64 rhs = left ? B.cols : B.rows;
+  const int P = g_prof.on ? 1 : panel_streams(rhs);
+  if (P <= 1) {
+    Recursion<T>(op, threshold, s, &g->events, &g->leaves).run(eff, A, B, 0);
+  } else {
+    // Right-hand-side panels on P streams (fork/join inside the capture):
+    // one panel's small kernels (leaves, short-K GEMMs) fill the SMs another
+    // panel's kernel tails leave idle.  Kernels are independent of the
+    // number of right-hand sides, so the result is bitwise the unsplit one;
+    // events and leaf order are those of the single logical call.
+    Recursion<T>(op, threshold, nullptr, &g->events, &g->leaves, true).run(eff, A, B, 0);
+    DeviceRes* resp;
+    if (capture) {  // the capture path already holds g_mu
+      resp = &device_res(dev);
+    } else {
+      std::lock_guard<std::mutex> lock(g_mu);
+      resp = &device_res(dev);
+    }
+    DeviceRes& res = *resp;
+    std::vector<cudaEvent_t> evs;
+    auto ev = [&]() {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      evs.push_back(e);
+      return e;
+    };
+    cudaEvent_t fork = ev();
+    cuda_check(cudaEventRecord(fork, s), "record fork");
+    const i64 w = ((rhs + P - 1) / P + 63) / 64 * 64;
+    for (int k = 0; k < P; ++k) {
+      const i64 r0 = k * w;
+      if (r0 >= rhs) break;
+      const i64 wi = r0 + w <= rhs ? w : rhs - r0;
+      const DView<T> panel = left ? B.sub(0, r0, B.rows, wi) : B.sub(r0, 0, wi, B.cols);
+      cudaStream_t sk = k == 0 ? s : res.aux[k - 1];
+      if (k > 0) cuda_check(cudaStreamWaitEvent(sk, fork, 0), "wait fork");
+      Recursion<T>(op, threshold, sk, nullptr, nullptr).run(eff, A, panel, 0);
+      if (k > 0) {
+        cudaEvent_t join = ev();
+        cuda_check(cudaEventRecord(join, sk), "record join");
+        cuda_check(cudaStreamWaitEvent(s, join, 0), "wait join");
+      }
+    }
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  }
   cudaError_t le = cudaGetLastError();
   if (capture) {
     cudaGraph_t graph = nullptr;

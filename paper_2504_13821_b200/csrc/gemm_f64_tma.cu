@@ -34,7 +34,7 @@ int env_int(const char* k, int d) {
 }  // namespace
 
 // A 2D column-major operand as a tensor map.  outer_contig: element (o, k)
-// at X[o + k*ld] (dims {O, K}, box {BO, 16}, no swizzle); else element (o, k)
+// at X[o + k*ld] (dims {O, K}, box {BO + 4, 16}, no swizzle); else element (o, k)
 // at X[k + o*ld] (dims {K, O}, box {16, BO}, 128-byte swizzle).
 bool encode_operand(CUtensorMap* map, const double* X, i64 ld, i64 O, i64 K, int BO, bool outer_contig) {
   EncodeFn enc = encoder();
@@ -44,7 +44,7 @@ bool encode_operand(CUtensorMap* map, const double* X, i64 ld, i64 O, i64 K, int
   if (outer_contig) {
     dims[0] = static_cast<cuuint64_t>(O);
     dims[1] = static_cast<cuuint64_t>(K);
-    box[0] = static_cast<cuuint32_t>(BO);
+    box[0] = static_cast<cuuint32_t>(BO + 4);  // padded k-rows (gemm_f64_tma.cuh)
     box[1] = dgemm_tma::kBK;
   } else {
     dims[0] = static_cast<cuuint64_t>(K);

@@ -14,21 +14,27 @@
 // of the stage is done).  No __syncthreads in the mainloop, no per-thread
 // address arithmetic for global loads.
 //
-// Shared layouts (8-byte elements):
-//   outer-contiguous operand (A NoTrans / B Trans): plain 2D box {BO, 16},
-//     element (o, k) at k*BO + o.  Fragment reads are 16-byte pairs
-//     (ld.shared.v2.f64): the mma row/column permutation below gives each
-//     thread two adjacent outer indices, so a warp reads 4 full 128-byte rows
-//     -- 4 wavefronts for 512 bytes, the minimum.
+// Shared layouts (8-byte elements) -- both conflict-free for the way the
+// LSU splits a warp's request (128-bit loads: four phases of 8 consecutive
+// lanes; 64-bit loads: two half-warps):
+//   outer-contiguous operand (A NoTrans / B Trans): 2D box {BO + 4, 16}, so
+//     a k-row is BO + 4 doubles long (the 4 extra outer elements are loaded
+//     and never used; this is the padding TMA cannot otherwise express).
+//     Each thread reads two adjacent outer indices with one ld.shared.v2.f64;
+//     a phase (2 outer pairs x 4 k-rows) then covers 8 distinct 16-byte bank
+//     groups because consecutive k-rows are shifted by 32 bytes.
 //   k-contiguous operand (A Trans / B NoTrans): 2D box {16, BO} with the
-//     128-byte TMA swizzle, element (o, k) at o*16 + 2*((k/2) ^ (o%8)) + k%2;
-//     8-byte fragment reads are conflict-free (2 wavefronts per 256 bytes).
+//     128-byte TMA swizzle, element (o, k) at o*16 + 2*((k/2) ^ (o%8)) + k%2.
+//     Fragment row g of an 8-row group is stored at outer index
+//     perm(g) = 2*(g%4) + g/4, so a half-warp (g = 0..3 or 4..7) meets four
+//     distinct (o%8)/2 values and its 16 loads land in 8 distinct chunks.
 //
 // Permutations (free: they only relabel which output row/column an mma
-// lane-slot holds, never the k order): for outer-contiguous A, mma row r of
-// 16-row tile i is m = 16i + 2(r%8) + r/8; for outer-contiguous B, the two
-// 8-column mma tiles 2q, 2q+1 interleave: column c of tile j is
-// n = 16q + 2c + (j%2).
+// lane-slot holds, never the k order): outer-contiguous A: mma row r of
+// 16-row tile i is m = 16i + 2(r%8) + r/8; k-contiguous A: m = 16i +
+// 8(r/8) + perm(r%8); outer-contiguous B: the 8-column mma tiles 2q, 2q+1
+// interleave, column c of tile j is n = 16q + 2c + (j%2); k-contiguous B:
+// n = 8j + perm(c).
 //
 // Determinism: each output element is accumulated over k in 16-wide k-tiles
 // of four m16n8k4 steps from a zero accumulator, then C = fma(alpha, acc,
@@ -104,8 +110,12 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
   constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
   constexpr int TM = WM / 16, TN = WN / 8;
   static_assert(WM % 16 == 0 && WN % 16 == 0, "warp tile");
-  constexpr uint32_t A_BYTES = BM * kBK * 8, B_BYTES = BN * kBK * 8;
-  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr int PAD = 4;  // extra outer elements per k-row of an outer-contiguous tile
+  constexpr int A_PITCH = MC_A ? BM + PAD : BM, B_PITCH = MC_B ? BN + PAD : BN;
+  constexpr uint32_t A_BYTES = A_PITCH * kBK * 8, B_BYTES = B_PITCH * kBK * 8;
+  // 1024-byte aligned tiles (128-byte swizzle atoms)
+  constexpr uint32_t A_SLOT = (A_BYTES + 1023u) & ~1023u, B_SLOT = (B_BYTES + 1023u) & ~1023u;
+  constexpr uint32_t STAGE_BYTES = A_SLOT + B_SLOT;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for the 128-byte swizzle atoms.
@@ -115,7 +125,7 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
   auto full_bar = [&](int s) { return bars + 8u * s; };
   auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
   auto stage_a = [&](int s) { return sbase + s * STAGE_BYTES; };
-  auto stage_b = [&](int s) { return sbase + s * STAGE_BYTES + A_BYTES; };
+  auto stage_b = [&](int s) { return sbase + s * STAGE_BYTES + A_SLOT; };
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
@@ -145,7 +155,7 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
 
   auto issue = [&](int kf) {  // one elected thread: fill stage kf % STAGES with k-tile kf
     const int s = kf % STAGES;
-    mbar_expect_tx(full_bar(s), STAGE_BYTES);
+    mbar_expect_tx(full_bar(s), A_BYTES + B_BYTES);
     // outer-contiguous: dims {O, K}, coords {o0, k0}; k-contiguous: {K, O}, {k0, o0}
     if (MC_A) tma_load_2d(stage_a(s), &mapA, m0, kf * kBK, full_bar(s));
     else tma_load_2d(stage_a(s), &mapA, kf * kBK, m0, full_bar(s));
@@ -173,15 +183,16 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
   // Byte offsets within a stage's A / B tile for k-step 0 (k-steps add a
   // constant for outer-contiguous tiles; k-contiguous tiles use xo[kk]).
   // k-contiguous swizzled element (o, k): o*128 + (((k>>1) ^ (o&7)) << 4) + (k&1)*8,
-  // with o&7 == g for every fragment row/column this thread reads.
+  // with o&7 == perm(g) for every fragment row/column this thread reads.
+  const int pg = ((g & 3) << 1) | (g >> 2);
   uint32_t xo[4];
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk)
-    xo[kk] = static_cast<uint32_t>(((((4 * kk + t) >> 1) ^ g) << 4) + (t & 1) * 8);
-  const uint32_t a_mc = static_cast<uint32_t>((t * BM + wm0 + 2 * g) * 8);
-  const uint32_t a_kc = static_cast<uint32_t>((wm0 + g) * 128);
-  const uint32_t b_mc = static_cast<uint32_t>((t * BN + wn0 + 2 * g) * 8);
-  const uint32_t b_kc = static_cast<uint32_t>((wn0 + g) * 128);
+    xo[kk] = static_cast<uint32_t>(((((4 * kk + t) >> 1) ^ pg) << 4) + (t & 1) * 8);
+  const uint32_t a_mc = static_cast<uint32_t>((t * A_PITCH + wm0 + 2 * g) * 8);
+  const uint32_t a_kc = static_cast<uint32_t>((wm0 + pg) * 128);
+  const uint32_t b_mc = static_cast<uint32_t>((t * B_PITCH + wn0 + 2 * g) * 8);
+  const uint32_t b_kc = static_cast<uint32_t>((wn0 + pg) * 128);
 
   double af[2][TM][2], bf[2][TN];
   auto load_frags = [&](int buf, int s, int kk) {
@@ -189,7 +200,7 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
       if (MC_A) {
-        lds128(af[buf][i][0], af[buf][i][1], as + a_mc + (kk * 4 * BM + 16 * i) * 8);
+        lds128(af[buf][i][0], af[buf][i][1], as + a_mc + (kk * 4 * A_PITCH + 16 * i) * 8);
       } else {
         lds64(af[buf][i][0], as + a_kc + xo[kk] + (16 * i) * 128);
         lds64(af[buf][i][1], as + a_kc + xo[kk] + (16 * i + 8) * 128);
@@ -198,7 +209,7 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
     if (MC_B) {
 #pragma unroll
       for (int q = 0; q < TN / 2; ++q)
-        lds128(bf[buf][2 * q], bf[buf][2 * q + 1], bs + b_mc + (kk * 4 * BN + 16 * q) * 8);
+        lds128(bf[buf][2 * q], bf[buf][2 * q + 1], bs + b_mc + (kk * 4 * B_PITCH + 16 * q) * 8);
     } else {
 #pragma unroll
       for (int j = 0; j < TN; ++j) lds64(bf[buf][j], bs + b_kc + xo[kk] + (8 * j) * 128);
@@ -253,14 +264,14 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const i64 m = m0 + wm0 + 16 * i + (MC_A ? 2 * g + h : 8 * h + g);
+      const i64 m = m0 + wm0 + 16 * i + (MC_A ? 2 * g + h : 8 * h + pg);
       if (m >= p.M) continue;
 #pragma unroll
       for (int j = 0; j < TN; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = 2 * t + e;
-          const i64 n = n0 + wn0 + (MC_B ? 16 * (j >> 1) + 2 * c + (j & 1) : 8 * j + c);
+          const i64 n = n0 + wn0 + (MC_B ? 16 * (j >> 1) + 2 * c + (j & 1) : 8 * j + (((c & 3) << 1) | (c >> 2)));
           if (n < p.N) {
             double* cp = p.C + m + n * p.ldc;
             const double v = acc[i][j][2 * h + e];

@@ -16,7 +16,9 @@ struct Config {
     if (!encode_operand(&ma, p.A, p.lda, p.M, p.K, BM, MC_A)) return false;
     if (!encode_operand(&mb, p.B, p.ldb, p.N, p.K, BN, MC_B)) return false;
     auto kern = dgemm_tma_kernel<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B>;
-    constexpr int smem = STAGES * (BM + BN) * kBK * 8 + 16 * STAGES + 1024;
+    constexpr int slot_a = ((MC_A ? BM + 4 : BM) * kBK * 8 + 1023) / 1024 * 1024;
+    constexpr int slot_b = ((MC_B ? BN + 4 : BN) * kBK * 8 + 1023) / 1024 * 1024;
+    constexpr int smem = STAGES * (slot_a + slot_b) + 16 * STAGES + 1024;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const unsigned grid = static_cast<unsigned>(ceil_div(p.M, BM) * ceil_div(p.N, BN));
     constexpr int threads = (WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32;

@@ -46,13 +46,17 @@ struct LeafParams {
   // Experiments only (RECTRI_CU_LEAF_DEBUG): 1 no diagonal part, 2 no GEMM
   // part (timing), 3 planted missing barrier (racecheck negative test).
   int debug_skip = 0;
+  long long* trace = nullptr;  // RECTRI_CU_LEAF_TRACE: per-CTA clock64 stamps (leaf64.cu)
 };
 
 constexpr int kLeafMax = 256;
 
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s);
 void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s);
-void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s);
+void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s);     // leaf64.cu (v2)
+void launch_leaf_f64_v1(const LeafParams<double>& p, cudaStream_t s);  // leaf.cu
+// Allocates the v2 fp64 leaf's per-stream scratch (call before capturing on s).
+void leaf_scratch_reserve(cudaStream_t s);
 void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s);
 
 // B[rows x cols] (ld) <- alpha * B.

@@ -1,0 +1,81 @@
+"""fp64 leaf kernel v2 (leaf64.cu: packed triangle, bulk-copy ring, solver
+warp) against leaf v1 (leaf.cu) -- identical per-element arithmetic, so the
+two must agree bit for bit on every variant, tile order, right-hand-side
+count and alpha; plus the oracle tolerance and the masking rules."""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2504_13821_b200 import NO_GRAPH, Backend, Threshold, rec_trmm, rec_trsm, trmm_base, trsm_base
+from tests._util import check_against_oracle, to_dev, to_np, tspec
+
+pytestmark = pytest.mark.gpu
+F = np.asfortranarray
+VARIANTS = list(itertools.product((0, 1), (0, 1), (0, 1), (0, 1)))  # side, uplo, trans, diag
+
+
+def _inputs(op, s, n, m, rng):
+    seed = int(rng.integers(1 << 30))
+    return F(oracle.make_operand(s, op == "trsm", n, seed)), F(oracle.make_rhs(s, n, m, seed + 1))
+
+
+def _base(op, s, a, b, version, monkeypatch, backend=None):
+    monkeypatch.setenv("RECTRI_CU_LEAF", str(version))
+    A, B = to_dev(a), to_dev(b)
+    fn = trmm_base if op == "trmm" else trsm_base
+    fn(tspec(s), A.cview(), B.view(), 256, backend or Backend.cuda(flags=NO_GRAPH))
+    return to_np(B)
+
+
+@pytest.mark.parametrize("op", ["trsm", "trmm"])
+@pytest.mark.parametrize("side,uplo,trans,diag", VARIANTS)
+def test_leaf_v2_bitwise_equals_v1(cuda, monkeypatch, op, side, uplo, trans, diag):
+    rng = np.random.default_rng(100 + 8 * side + 4 * uplo + 2 * trans + diag)
+    for n, m, alpha in ((1, 3, 1.0), (5, 33, 1.0), (32, 32, 2.5), (33, 70, 1.0), (100, 65, -0.75),
+                        (256, 96, 1.0), (255, 31, 1.0)):
+        s = oracle.spec(side, uplo, trans, diag, alpha)
+        a, b = _inputs(op, s, n, m, rng)
+        v1 = _base(op, s, a, b, 1, monkeypatch)
+        v2 = _base(op, s, a, b, 2, monkeypatch)
+        assert oracle.bitwise_equal(v1, v2), (op, side, uplo, trans, diag, n, m, alpha)
+        if n <= 100:
+            check_against_oracle(op, s, a, b, v2)
+
+
+@pytest.mark.parametrize("op", ["trsm", "trmm"])
+def test_leaf_v2_in_captured_recursion(cuda, monkeypatch, op):
+    """The recursion's CUDA graph (leaves on the capture and panel streams)
+    with the v2 leaf equals direct launches with the v1 leaf, bitwise."""
+    rng = np.random.default_rng(7)
+    n, m = 1024, 4100
+    s = oracle.spec(0, 0, 0, 0, 1.0)
+    a, b = _inputs(op, s, n, m, rng)
+    fn = rec_trmm if op == "trmm" else rec_trsm
+    outs = []
+    for version, be in ((1, Backend.cuda(flags=NO_GRAPH)), (2, Backend.cuda())):
+        monkeypatch.setenv("RECTRI_CU_LEAF", str(version))
+        A, B = to_dev(a), to_dev(b)
+        fn(tspec(s), A.cview(), B.view(), Threshold(256), be)
+        outs.append(to_np(B))
+    assert oracle.bitwise_equal(outs[0], outs[1])
+
+
+def test_leaf_v2_masking_and_alpha_zero(cuda, monkeypatch):
+    rng = np.random.default_rng(3)
+    n, m = 100, 40
+    for uplo in (0, 1):
+        s = oracle.spec(0, uplo, 0, 1, 1.0)  # Unit: the stored diagonal is never read
+        a, b = _inputs("trsm", s, n, m, rng)
+        junk = a.copy()
+        iu = np.triu_indices(n, 1) if uplo == 0 else np.tril_indices(n, -1)
+        junk[iu] = np.nan
+        np.fill_diagonal(junk, np.nan)
+        ref = _base("trsm", s, a, b, 2, monkeypatch)
+        got = _base("trsm", s, junk, b, 2, monkeypatch)
+        assert np.all(np.isfinite(got)) and oracle.bitwise_equal(ref, got)
+    s = oracle.spec(0, 0, 0, 0, 0.0)
+    b = F(np.full((n, m), np.nan))
+    got = _base("trmm", s, F(rng.uniform(-1, 1, (n, n))), b, 2, monkeypatch)
+    assert np.all(got == 0.0)
