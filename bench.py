@@ -419,12 +419,15 @@ def main():
                 walls.append(w)
         wall = allmax(sum(walls), world)
         e2e = {"value": float(n) * n * me * world * args.steps / wall / 1e9, "unit": "GFLOP/s",
-               # A: stored triangle as 512-column trapezoids (driver.cu copy_triangle_h2d)
-               "h2d_bytes_per_step": (sum((n - c0) * min(512, n - c0) for c0 in range(0, n, 512)) + n * me) * 8 * world,
+               # A: the recursion's leaf diagonal blocks (full squares) + off-diagonal GEMM blocks,
+               # (n^2 + n t)/2 elements (driver.cu run_host_streamed); B: every element once
+               "h2d_bytes_per_step": ((n * n + n * args.threshold) // 2 + n * me) * 8 * world,
                "d2h_bytes_per_step": n * me * 8 * world,
                "rhs_per_gpu": me,
                "ms_per_step": wall / args.steps * 1e3,
-               "path": "rectri_cu_rec_trsm_f64 with pinned host views (H2D A+B, compute, D2H B), wall clock"}
+               "path": "rectri_cu_rec_trsm_f64 with pinned host views: A blocks and B row chunks copied in "
+                       "first-use order, each kernel gated on its own inputs, chunks copied back after their "
+                       "last writer (driver.cu run_host_streamed); wall clock"}
         log(f"e2e: {e2e['value']:.1f} GFLOP/s")
         del Ah, Bh, Bh0
 

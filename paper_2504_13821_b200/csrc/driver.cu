@@ -10,11 +10,13 @@
 // recorded event list replayed to the caller's sink.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <list>
 #include <map>
 #include <memory>
@@ -278,12 +280,31 @@ void enqueue_gemm(T alpha, bool ta, DView<const T> A, bool tb, DView<const T> B,
 template <typename T>
 void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s);
 
+// One kernel of the recursion, as emitted by a descriptor run (the streamed
+// host path executes these itself).
+template <typename T>
+struct KDesc {
+  bool leaf;
+  Spec spec;             // leaf: the (alpha-adjusted) spec
+  DView<const T> a;      // leaf: diagonal block; GEMM: off-diagonal block
+  DView<T> src, dst;     // leaf: dst = its B block; GEMM: src (read), dst (updated)
+  T coeff;               // GEMM: dst += coeff * op(off) * src  (Right: src * op(off))
+  bool off_trans, off_on_left;
+};
+
 template <typename T>
 class Recursion {
  public:
   Recursion(OpK op, i64 threshold, cudaStream_t s, std::vector<Ev>* events,
             std::vector<std::pair<i64, i64>>* leaves, bool dry = false)
       : op_(op), threshold_(threshold), s_(s), events_(events), leaves_(leaves), dry_(dry) {}
+
+  // Called before each kernel (also in dry runs): leaf (a = diagonal block,
+  // b1 = its B block, b2 unused) or GEMM (a = off-diagonal block, b1 = src,
+  // b2 = dst).
+  std::function<void(bool leaf, DView<const T> a, DView<T> b1, DView<T> b2)> before;
+  // Descriptor mode: every kernel is handed to `kernels` instead of launched.
+  std::function<void(const KDesc<T>&)> kernels;
 
   // recursion.cpp:85-148
   void run(const Spec& spec, DView<const T> A, DView<T> B, i64 row0) {
@@ -292,7 +313,9 @@ class Recursion {
     if (n <= threshold_) {
       emit(op_ == kTrmm ? RECTRI_CU_EV_BASE_TRMM : RECTRI_CU_EV_BASE_TRSM, n, rhs);
       if (leaves_) leaves_->push_back({row0, n});
-      if (!dry_) enqueue_base<T>(op_, spec, A, B, s_);
+      if (before) before(true, A, B, B);
+      if (kernels) kernels(KDesc<T>{true, spec, A, B, B, T(0), false, false});
+      else if (!dry_) enqueue_base<T>(op_, spec, A, B, s_);
       return;
     }
     const i64 mid = n / 2;  // split_half
@@ -312,7 +335,10 @@ class Recursion {
     const DView<const T> src = sc.read_b2 ? b2 : b1;
     const T coeff = static_cast<T>(sc.sign * (sc.carries_alpha ? spec.alpha : 1.0));
     emit(RECTRI_CU_EV_GEMM, dst.rows, dst.cols);
-    if (dry_) {
+    if (before) before(false, off, sc.read_b2 ? b2 : b1, dst);
+    if (kernels) {
+      kernels(KDesc<T>{false, spec, off, sc.read_b2 ? b2 : b1, dst, coeff, sc.off_trans != 0, sc.off_on_left});
+    } else if (dry_) {
     } else if (sc.off_on_left)
       enqueue_gemm<T>(coeff, sc.off_trans != 0, off, false, src, T(1), dst, s_);
     else
@@ -681,9 +707,11 @@ void run_host_panels(OpK op, const Spec& spec, DView<const T> dA, DView<T> hB, i
   const bool left = spec.side == RECTRI_CU_LEFT;
   const i64 n = dA.rows;
   const i64 rhs = left ? hB.cols : hB.rows;
-  // Panel width: a few panels for overlap, none narrower than 2048.
+  // Panel width: a few panels for overlap, none narrower than 2048
+  // (RECTRI_CU_HOST_PANEL overrides, for tuning).
   i64 w = (rhs + 3) / 4;
   if (w < 2048) w = 2048;
+  if (const char* e = getenv("RECTRI_CU_HOST_PANEL")) w = atoll(e) > 0 ? atoll(e) : w;
   if (w > rhs) w = rhs;
   const i64 np = (rhs + w - 1) / w;
 
@@ -752,6 +780,295 @@ void run_host_panels(OpK op, const Spec& spec, DView<const T> dA, DView<T> hB, i
   if (first) raise_if_singular(*first);
 }
 
+// Host-resident B (and optionally A), whole problem resident on the device:
+// A's blocks and B's row chunks (Right side: column chunks) are copied H2D in
+// the order the recursion first touches them, each kernel waits only for its
+// own inputs, and each B chunk is copied back as soon as its last writer has
+// run -- so the transfers hide under the compute except the first chunk's
+// copy-in and the last chunk's copy-back.  GEMM updates whose destination
+// spans several chunks are split at chunk boundaries (a split of the M
+// dimension -- Right side: N -- never changes an element's arithmetic), so
+// e.g. the level-1 update starts on the first chunk that has arrived.  Same
+// kernels, same per-element order as the device path (bitwise the same
+// result); the event sink sees the single logical call.  Returns false
+// (nothing done) when the device cannot hold the problem; the caller then
+// uses run_host_panels.
+template <typename T>
+bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, DView<T> hB, i64 threshold,
+                       const BackendInfo& be, rectri_cu_event_fn sink, void* user, int dev) {
+  const bool left = spec.side == RECTRI_CU_LEFT;
+  const i64 n = A.rows, brows = hB.rows, bcols = hB.cols;
+  const size_t bbytes = static_cast<size_t>(brows * bcols) * sizeof(T);
+  const size_t abytes = a_dev ? 0 : static_cast<size_t>(n * n) * sizeof(T);
+  DeviceRes* res;
+  T* dAp = nullptr;
+  T* dBp = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    res = &device_res(dev);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t have = (a_dev ? 0 : res->stage_bytes[0]) + res->stage_bytes[1];
+    const size_t room = free_b + have > (size_t{1} << 30) ? free_b + have - (size_t{1} << 30) : 0;
+    if (abytes + bbytes > room) return false;
+    if (!a_dev) dAp = static_cast<T*>(staging(*res, 0, abytes));
+    dBp = static_cast<T*>(staging(*res, 1, bbytes));
+  }
+  const DView<const T> dA = a_dev ? A : DView<const T>{dAp, n, n, n};
+  const DView<T> dB{dBp, brows, brows, bcols};
+  Spec eff = spec;
+  if (op == kTrsm) eff.alpha = 1.0;
+
+  // Descriptor run: the recursion's kernels in order (and its events, leaves).
+  std::vector<Ev> evs_logical;
+  std::vector<std::pair<i64, i64>> leaves;
+  std::vector<KDesc<T>> ks;
+  {
+    Recursion<T> dry(op, threshold, nullptr, &evs_logical, &leaves, true);
+    dry.kernels = [&](const KDesc<T>& k) { ks.push_back(k); };
+    dry.run(eff, dA, dB, 0);
+  }
+  if (sink)
+    for (const Ev& e : evs_logical) sink(user, e.e, e.n, e.m);
+
+  // B chunks along the triangle dimension: consecutive leaves merged to
+  // >= 1024 rows (columns, Right).
+  std::vector<std::pair<i64, i64>> lv = leaves;
+  std::sort(lv.begin(), lv.end());
+  std::vector<i64> cb{0};
+  const char* ce = getenv("RECTRI_CU_E2E_CHUNK");  // tuning knob (rows per chunk)
+  const i64 chunk_min = ce && atoll(ce) > 0 ? atoll(ce) : 1024;
+  for (const auto& l : lv) {
+    // small chunks at both ends of the triangle dimension: the first copy-in
+    // and the last copy-back are the transfers no compute hides
+    const i64 end = l.first + l.second;
+    const i64 want = (end <= chunk_min || end > n - chunk_min) ? chunk_min / 4 : chunk_min;
+    if (end - cb.back() >= want || end == n) cb.push_back(end);
+  }
+  const int nch = static_cast<int>(cb.size()) - 1;
+  auto off_of = [&](const T* p) { return left ? static_cast<i64>(p - dB.p) : static_cast<i64>(p - dB.p) / dB.ld; };
+  auto len_of = [&](const DView<T>& v) { return left ? v.rows : v.cols; };
+  auto chunk_of = [&](i64 r) {
+    return static_cast<int>(std::upper_bound(cb.begin(), cb.end(), r) - cb.begin()) - 1;
+  };
+  auto b_chunk = [&](DView<T> base, int c) {
+    return left ? base.sub(cb[c], 0, cb[c + 1] - cb[c], bcols) : base.sub(0, cb[c], brows, cb[c + 1] - cb[c]);
+  };
+
+  // Unit kernels: leaves as they are, GEMMs split at dst chunk boundaries.
+  struct Unit {
+    const KDesc<T>* k;
+    DView<const T> a;  // the A block this unit reads (GEMM: its slice of off)
+    DView<T> dst;      // the B range it writes
+    i64 s0, s1;        // B range it reads besides dst (GEMM src), triangle coords
+  };
+  std::vector<Unit> units;
+  for (const KDesc<T>& k : ks) {
+    if (k.leaf) {
+      units.push_back(Unit{&k, k.a, k.dst, 0, 0});
+      continue;
+    }
+    const i64 d0 = off_of(k.dst.p), dl = len_of(k.dst);
+    const i64 s0 = off_of(k.src.p), s1 = s0 + len_of(k.src);
+    for (int c = chunk_of(d0); c < nch && cb[c] < d0 + dl; ++c) {
+      const i64 lo = std::max(cb[c], d0) - d0, hi = std::min(cb[c + 1], d0 + dl) - d0;
+      const i64 h = hi - lo;
+      DView<T> dsub = left ? k.dst.sub(lo, 0, h, k.dst.cols) : k.dst.sub(0, lo, k.dst.rows, h);
+      // slice of op(off) feeding those dst rows (Left) / columns (Right)
+      DView<const T> asub = left ? (k.off_trans ? k.a.sub(0, lo, k.a.rows, h) : k.a.sub(lo, 0, h, k.a.cols))
+                                 : (k.off_trans ? k.a.sub(lo, 0, h, k.a.cols) : k.a.sub(0, lo, k.a.rows, h));
+      units.push_back(Unit{&k, asub, dsub, s0, s1});
+    }
+  }
+  std::vector<int> last_writer(nch, -1);
+  for (int i = 0; i < static_cast<int>(units.size()); ++i) {
+    const i64 w0 = off_of(units[i].dst.p), w1 = w0 + len_of(units[i].dst);
+    for (int c = chunk_of(w0); c < nch && cb[c] < w1; ++c) last_writer[c] = i;
+  }
+
+  const bool scan = op == kTrsm && spec.diag == RECTRI_CU_NONUNIT;
+  uint8_t* d_flags = nullptr;
+  uint8_t* h_flags = nullptr;
+  std::vector<uint8_t> flags;
+  cudaStream_t cs = be.stream, hs = res->h2d, ds = res->d2h;
+  std::vector<cudaEvent_t> evs;
+  auto ev = [&]() {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    evs.push_back(e);
+    return e;
+  };
+  auto copy2d = [&](T* dst, i64 dld, const T* src, i64 sld, i64 rows, i64 cols, cudaMemcpyKind kind,
+                    cudaStream_t st) {
+    cuda_check(cudaMemcpy2DAsync(dst, sizeof(T) * dld, src, sizeof(T) * sld, sizeof(T) * rows, cols, kind, st),
+               "staged copy");
+  };
+  const bool trace = getenv("RECTRI_CU_E2E_TRACE") != nullptr;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> d2h_marks;
+  try {
+    cudaEvent_t start;
+    cuda_check(cudaEventCreate(&start), "event");  // timed (RECTRI_CU_E2E_TRACE)
+    evs.push_back(start);
+    cuda_check(cudaEventRecord(start, cs), "record");  // staging buffers free (stream order)
+    cuda_check(cudaStreamWaitEvent(hs, start, 0), "wait");
+    if (scan && a_dev) {
+      cuda_check(cudaMalloc(&d_flags, static_cast<size_t>(n)), "flags alloc");
+      cuda_check(cudaMallocHost(&h_flags, static_cast<size_t>(n)), "flags alloc");
+      K<T>::scan(A.p, A.ld, n, d_flags, cs);
+      cuda_check(cudaMemcpyAsync(h_flags, d_flags, static_cast<size_t>(n), cudaMemcpyDeviceToHost, cs), "flags");
+    }
+    // H2D in first-use order; ready[i] gates unit i.
+    std::vector<cudaEvent_t> ready(units.size(), nullptr);
+    std::vector<std::vector<int>> fresh(units.size());  // chunks first loaded for unit i
+    std::vector<char> loaded(nch, 0);
+    for (size_t i = 0; i < units.size(); ++i) {
+      const Unit& u = units[i];
+      bool issued = false;
+      if (!a_dev) {  // device sub-view; the host block sits at the same offsets
+        const i64 off = static_cast<i64>(u.a.p - dA.p);
+        copy2d(const_cast<T*>(u.a.p), n, A.p + off % n + (off / n) * A.ld, A.ld, u.a.rows, u.a.cols,
+               cudaMemcpyHostToDevice, hs);
+        issued = true;
+      }
+      const i64 w0 = off_of(u.dst.p), w1 = w0 + len_of(u.dst);
+      for (int pass = 0; pass < 2; ++pass) {
+        const i64 r0 = pass ? u.s0 : w0, r1 = pass ? u.s1 : w1;
+        for (int c = chunk_of(r0); r1 > r0 && c < nch && cb[c] < r1; ++c) {
+          if (loaded[c]) continue;
+          loaded[c] = 1;
+          const DView<T> d = b_chunk(dB, c), h = b_chunk(hB, c);
+          copy2d(d.p, d.ld, h.p, h.ld, d.rows, d.cols, cudaMemcpyHostToDevice, hs);
+          fresh[i].push_back(c);
+          issued = true;
+        }
+      }
+      if (issued) {
+        ready[i] = ev();
+        cuda_check(cudaEventRecord(ready[i], hs), "record");
+      }
+    }
+    if (scan && !a_dev) {  // host-side zero-pivot scan (trsm_base scans before writing)
+      flags.resize(static_cast<size_t>(n));
+      for (i64 r = 0; r < n; ++r) flags[r] = A.p[r + r * A.ld] == T(0) ? 1 : 0;
+    }
+    // Compute: each unit after its inputs, its right-hand sides split over P
+    // streams (as the device path's graph); chunk copy-back after its last
+    // writer on every stream.
+    const i64 rhs = left ? bcols : brows;
+    const int P = panel_streams(rhs);
+    const i64 pw = ((rhs + P - 1) / P + 63) / 64 * 64;
+    std::vector<cudaStream_t> ps(P);
+    for (int q = 0; q < P; ++q) ps[q] = q == 0 ? cs : res->aux[q - 1];
+    if (P > 1) {
+      cudaEvent_t fork = ev();
+      cuda_check(cudaEventRecord(fork, cs), "record");
+      for (int q = 1; q < P; ++q) cuda_check(cudaStreamWaitEvent(ps[q], fork, 0), "wait");
+    }
+    auto rhs_part = [&](DView<T> v, int q) {  // right-hand sides [q*pw, (q+1)*pw) of a B view
+      const i64 r0 = q * pw, r1 = std::min(rhs, r0 + pw);
+      return left ? v.sub(0, r0, v.rows, r1 - r0) : v.sub(r0, 0, r1 - r0, v.cols);
+    };
+    for (size_t i = 0; i < units.size(); ++i) {
+      const Unit& u = units[i];
+      const KDesc<T>& k = *u.k;
+      for (int q = 0; q < P && q * pw < rhs; ++q) {
+        cudaStream_t sq = ps[q];
+        if (ready[i]) cuda_check(cudaStreamWaitEvent(sq, ready[i], 0), "wait input");
+        if (op == kTrsm && spec.alpha != 1.0)  // alpha once per element, at first arrival
+          for (int c : fresh[i]) {
+            const DView<T> d = rhs_part(b_chunk(dB, c), q);
+            K<T>::scale(d.p, d.ld, d.rows, d.cols, static_cast<T>(spec.alpha), sq);
+          }
+        const DView<T> dst = rhs_part(u.dst, q);
+        if (k.leaf) {
+          enqueue_base<T>(op, k.spec, k.a, dst, sq);
+        } else if (k.off_on_left) {
+          enqueue_gemm<T>(k.coeff, k.off_trans, u.a, false, rhs_part(k.src, q), T(1), dst, sq);
+        } else {
+          enqueue_gemm<T>(k.coeff, false, rhs_part(k.src, q), k.off_trans, u.a, T(1), dst, sq);
+        }
+      }
+      for (int c = 0; c < nch; ++c) {
+        if (last_writer[c] != static_cast<int>(i)) continue;
+        for (int q = 0; q < P && q * pw < rhs; ++q) {
+          cudaEvent_t done = ev();
+          cuda_check(cudaEventRecord(done, ps[q]), "record");
+          cuda_check(cudaStreamWaitEvent(ds, done, 0), "wait");
+        }
+        const DView<T> d = b_chunk(dB, c), h = b_chunk(hB, c);
+        if (trace) {
+          cudaEvent_t e0, e1;
+          cudaEventCreate(&e0);
+          cudaEventCreate(&e1);
+          evs.push_back(e0);
+          evs.push_back(e1);
+          cudaEventRecord(e0, ds);
+          copy2d(h.p, h.ld, d.p, d.ld, d.rows, d.cols, cudaMemcpyDeviceToHost, ds);
+          cudaEventRecord(e1, ds);
+          d2h_marks.push_back({c, {e0, e1}});
+        } else {
+          copy2d(h.p, h.ld, d.p, d.ld, d.rows, d.cols, cudaMemcpyDeviceToHost, ds);
+        }
+      }
+    }
+    for (int q = 1; q < P; ++q) {  // join
+      cudaEvent_t join = ev();
+      cuda_check(cudaEventRecord(join, ps[q]), "record");
+      cuda_check(cudaStreamWaitEvent(cs, join, 0), "wait");
+    }
+    cuda_check(cudaGetLastError(), "kernel launch");
+    cudaEvent_t t_end[3] = {nullptr, nullptr, nullptr};
+    if (trace) {
+      for (int q = 0; q < 3; ++q) {
+        cudaEventCreate(&t_end[q]);
+        evs.push_back(t_end[q]);
+      }
+      cudaEventRecord(t_end[0], hs);
+      cudaEventRecord(t_end[1], cs);
+      cudaEventRecord(t_end[2], ds);
+    }
+    cuda_check(cudaStreamSynchronize(ds), "synchronize");
+    cuda_check(cudaStreamSynchronize(cs), "synchronize");
+    cuda_check(cudaStreamSynchronize(hs), "synchronize");
+    if (trace) {
+      float t[3] = {0, 0, 0};
+      for (int q = 0; q < 3; ++q) cudaEventElapsedTime(&t[q], start, t_end[q]);
+      fprintf(stderr, "e2e trace: h2d done %.2f ms, compute done %.2f ms, d2h done %.2f ms, %zu units, %d chunks\n",
+              t[0], t[1], t[2], units.size(), nch);
+      for (const auto& mk : d2h_marks) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, start, mk.second.first);
+        cudaEventElapsedTime(&b, start, mk.second.second);
+        fprintf(stderr, "  d2h chunk %d rows [%lld, %lld): %.2f -> %.2f ms\n", mk.first, (long long)cb[mk.first],
+                (long long)cb[mk.first + 1], a, b);
+      }
+    }
+  } catch (...) {
+    cudaStreamSynchronize(hs);
+    cudaStreamSynchronize(ds);
+    cudaStreamSynchronize(cs);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    if (d_flags) cudaFree(d_flags);
+    if (h_flags) cudaFreeHost(h_flags);
+    throw;
+  }
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  if (h_flags) {
+    flags.assign(h_flags, h_flags + n);
+    cudaFree(d_flags);
+    cudaFreeHost(h_flags);
+  }
+  if (!flags.empty())
+    for (const auto& leaf : leaves)
+      for (i64 r = leaf.first; r < leaf.first + leaf.second; ++r)
+        if (flags[static_cast<size_t>(r)]) {
+          Fail f{RECTRI_CU_SINGULAR, "singular triangular matrix: zero diagonal at row " + std::to_string(r)};
+          f.index = r;
+          throw f;
+        }
+  return true;
+}
+
 // rec_trmm / rec_trsm entry (recursion.cpp:165-192).
 template <typename T>
 void rec_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
@@ -805,6 +1122,9 @@ void rec_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
     run_device<T>(op, spec, dA, B, threshold, be2, sink, user, dev, true);
     return;
   }
+  if (!getenv("RECTRI_CU_HOST_PANEL") &&
+      run_host_streamed<T>(op, spec, A, a_dev, B, threshold, be2, sink, user, dev))
+    return;
   cudaEvent_t a_ready = nullptr;
   if (!a_dev) {
     copy_triangle_h2d<T>(const_cast<T*>(dA.p), A, spec.uplo, res->h2d);

@@ -335,3 +335,46 @@ def test_host_staged_equals_device(cuda):
     B.data = B.data.pin_memory()
     rec_trsm(tspec(s), A.cview(), B.view(), Threshold(64))
     assert oracle.bitwise_equal(dev, to_np(B))
+
+
+@pytest.mark.parametrize("op", ["trsm", "trmm"])
+def test_host_streamed_all_variants(cuda, op, monkeypatch):
+    """Host views take the first-use streamed path (A blocks and B chunks
+    copied in, chunks copied back after their last writer): bitwise the
+    device result for every variant, with several B chunks, alpha != 1, a
+    device A with a host B, and the panelled fallback."""
+    n, m = 2600, 96
+    for side, uplo, trans, diag in [(0, 0, 0, 0), (0, 1, 1, 1), (1, 0, 1, 0), (1, 1, 0, 1), (0, 1, 0, 0), (1, 0, 0, 1)]:
+        s = oracle.spec(side, uplo, trans, diag, 1.5)
+        a = oracle.make_operand(s, op == "trsm", n, 11)
+        b = oracle.make_rhs(s, n, m, 12)
+        dev = run_op(op, s, a, b, 256)
+        evs_dev, evs_host = [], []
+        host = run_op(op, s, a, b, 256, device="cpu", sink=lambda e, nn, mm: evs_host.append((int(e), nn, mm)))
+        run_op(op, s, a, b, 256, sink=lambda e, nn, mm: evs_dev.append((int(e), nn, mm)))
+        assert oracle.bitwise_equal(dev, host), (side, uplo, trans, diag)
+        assert evs_dev == evs_host
+        # device A, host B
+        A = to_dev(a)
+        B = MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(b)), device="cpu")
+        fn = rec_trmm if op == "trmm" else rec_trsm
+        fn(tspec(s), A.cview(), B.view(), Threshold(256))
+        assert oracle.bitwise_equal(dev, to_np(B))
+    monkeypatch.setenv("RECTRI_CU_HOST_PANEL", "40")  # panelled fallback
+    s = oracle.spec(0, 0, 0, 0, 1.0)
+    a = oracle.make_operand(s, op == "trsm", n, 13)
+    b = oracle.make_rhs(s, n, m, 14)
+    assert oracle.bitwise_equal(run_op(op, s, a, b, 256), run_op(op, s, a, b, 256, device="cpu"))
+
+
+def test_host_streamed_singular(cuda):
+    n = 2100
+    s = oracle.spec(0, 0, 0, 0, 1.0)
+    a = oracle.make_operand(s, True, n, 3)
+    a[1500, 1500] = 0.0
+    b = oracle.make_rhs(s, n, 8, 4)
+    A = MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(a)), device="cpu")
+    B = MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(b)), device="cpu")
+    with pytest.raises(SingularityError) as ei:
+        rec_trsm(tspec(s), A.cview(), B.view(), Threshold(256))
+    assert ei.value.index() == 1500

@@ -37,7 +37,8 @@ def test_kernels_clean(cuda, tool, args):
 
 
 def test_planted_race_is_detected(cuda):
-    r = _san("racecheck", ["leaf", "100", "70"], {"RECTRI_CU_LEAF_DEBUG": "3"})
+    # the planted missing barrier lives in the v1 leaf (leaf.cu)
+    r = _san("racecheck", ["leaf", "100", "70"], {"RECTRI_CU_LEAF_DEBUG": "3", "RECTRI_CU_LEAF": "1"})
     out = r.stdout + r.stderr
     m = re.search(r"RACECHECK SUMMARY: (\d+) hazards displayed \((\d+) errors", out)
     assert m and int(m.group(1)) > 0 and int(m.group(2)) > 0, out[-3000:]
