@@ -55,6 +55,7 @@ void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t
 void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s);
 void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s);     // leaf64.cu (v2)
 void launch_leaf_f64_v1(const LeafParams<double>& p, cudaStream_t s);  // leaf.cu
+void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream_t s);  // leaf64_v3.cu
 // Allocates the v2 fp64 leaf's per-stream scratch (call before capturing on s).
 void leaf_scratch_reserve(cudaStream_t s);
 void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s);

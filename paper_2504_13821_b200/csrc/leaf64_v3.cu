@@ -1,0 +1,286 @@
+// leaf64_v3.cu -- fp64 base (leaf) kernel v3: every step on the DMMA pipe.
+//
+// trsm_base / trmm_base (src/base_kernels.cpp:94-177) on the Left form of a
+// virtual lower factor L' (reflected / transposed indices),
+// blocked in 32-row blocks.  Differs from v1/v2 (leaf.cu / leaf64.cu) only in
+// how the 32x32 diagonal block is applied:
+//   TRSM: X_I = inv(L'_II) * (b_I - sum_{J<I} L'_IJ X_J).  inv(L'_II) is
+//         computed once per leaf call by pack3_kernel (forward substitution
+//         of the 32 unit vectors, one thread per column, divisions as in the
+//         reference's trsm_left_lower) and applied as a 32x32x32 DMMA
+//         product, so no 32-step dependency chain sits in the consumer.
+//   TRMM: X_I = alpha * (sum_{J<I} L'_IJ b_J + L'_II b_I) with L'_II carrying
+//         its diagonal (1 for Unit) -- one more DMMA block.
+// The results agree with v1/v2 to rounding (tolerance-checked, not bitwise:
+// the diagonal block's sums are re-associated); v1/v2 remain selectable
+// (RECTRI_CU_LEAF=1/2) for the reference's exact substitution order.
+//
+// pack3_kernel writes, per leaf call, the blocks in consumption order in
+// DMMA A-fragment order ([row tile mt][lane][k-step], 2 KB contiguous per
+// warp): TRSM row I: L'_I0 .. L'_I,I-1, then -inv(L'_II); TRMM (rows
+// descending) row I: L'_I0 .. L'_I,I-1, then L'_II.  Masked / out-of-range
+// entries are exact zeros by selection; padding rows beyond n get an
+// identity diagonal so every diagonal block is invertible.
+//
+// leaf3_kernel: one CTA owns 32 right-hand sides (panel nb x 32 in shared
+// memory, loaded once, written back once); 8 warps each own two m8n8 output
+// tiles of the current row block; A fragments stream from the (L2-resident)
+// scratch straight into registers one block ahead.  Per row block: GEMM
+// part, (TRSM) the negated partial result to shared memory + barrier, the
+// diagonal-block product, store + barrier.
+#include <cstdlib>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace rectri_cu {
+namespace leaf64v3 {
+
+constexpr int kRB = 32;
+constexpr int kNC = 32;
+constexpr int kThreads = 256;
+constexpr int kBlk = kRB * kRB;
+constexpr int kMaxBlk = kLeafMax / kRB;
+constexpr size_t kScratchDoubles = static_cast<size_t>(kMaxBlk * (kMaxBlk + 1) / 2) * kBlk;
+
+__device__ __forceinline__ int panel_idx(int r, int c) { return swz64(r, c, kNC); }
+
+__device__ __forceinline__ double lprime(const LeafParams<double>& p, int r, int j) {
+  const int rr = p.reflected ? p.n - 1 - r : r;
+  const int jj = p.reflected ? p.n - 1 - j : j;
+  const i64 row = p.swapped ? jj : rr;
+  const i64 col = p.swapped ? rr : jj;
+  return p.A[row + col * p.lda];
+}
+
+// Fragment order position of element (r, k) of a 32x32 block.
+__device__ __forceinline__ int frag_pos(int r, int k) {
+  const int mt = r >> 3, g = r & 7, kk = k >> 2, t = k & 3;
+  return (mt * 32 + 4 * g + t) * 8 + kk;
+}
+
+// Consumption index of block (I, J) (J == I: the diagonal block).
+__device__ __forceinline__ int seq_of(int I, int J, int nblk, bool asc) {
+  if (asc) return I * (I + 1) / 2 + J;
+  // rows nblk-1 .. I+1 come first; row I' holds I'+1 blocks
+  return (nblk * (nblk + 1) / 2 - (I + 1) * (I + 2) / 2) + J;
+}
+
+__global__ void __launch_bounds__(256) pack3_kernel(const LeafParams<double> p, double* __restrict__ P) {
+  __shared__ double L[kRB][kRB + 1];
+  const int nblk = (p.n + kRB - 1) / kRB;
+  const bool trsm = p.trsm != 0;
+  // blockIdx.x -> (I, J), J <= I, canonical ascending numbering
+  const int b = blockIdx.x;
+  int I = 0;
+  while ((I + 1) * (I + 2) / 2 <= b) ++I;
+  const int J = b - I * (I + 1) / 2;
+  const int r0 = I * kRB, j0 = J * kRB;
+  double* dst = P + static_cast<size_t>(seq_of(I, J, nblk, trsm)) * kBlk;
+  const int tid = threadIdx.x;
+  if (J < I) {
+    for (int o = tid; o < kBlk; o += blockDim.x) {
+      const int kk = o & 7, ln = (o >> 3) & 31, mt = o >> 8;
+      const int r = 8 * mt + (ln >> 2), k = 4 * kk + (ln & 3);
+      dst[o] = r0 + r < p.n ? lprime(p, r0 + r, j0 + k) : 0.0;
+    }
+    return;
+  }
+  // diagonal block: lower triangle with its diagonal (1 for Unit; identity
+  // on padding rows), zeros above
+  for (int o = tid; o < kBlk; o += blockDim.x) {
+    const int r = o >> 5, k = o & 31;
+    double v = 0.0;
+    if (r0 + r >= p.n) v = r == k ? 1.0 : 0.0;
+    else if (k < r) v = lprime(p, r0 + r, r0 + k);
+    else if (k == r) v = p.unit ? 1.0 : lprime(p, r0 + r, r0 + r);
+    L[r][k] = v;
+  }
+  __syncthreads();
+  if (!trsm) {
+    for (int o = tid; o < kBlk; o += blockDim.x) {
+      const int r = o >> 5, k = o & 31;
+      dst[frag_pos(r, k)] = L[r][k];
+    }
+    return;
+  }
+  // -inv(L): thread j solves L y = e_j by forward substitution
+  // (base_kernels.cpp:73-88 order: y_r = (e_r - sum_{p<r} L(r,p) y_p) / d_r).
+  if (tid < kRB) {
+    const int j = tid;
+    double y[kRB];
+#pragma unroll
+    for (int r = 0; r < kRB; ++r) {
+      double s = r == j ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < r; ++q) s = fma(-L[r][q], y[q], s);
+      y[r] = r < j ? 0.0 : s / L[r][r];
+    }
+#pragma unroll
+    for (int r = 0; r < kRB; ++r) dst[frag_pos(r, j)] = -y[r];
+  }
+}
+
+constexpr int kSmem = (kLeafMax * kNC + kRB * kNC) * 8;
+
+__global__ void __launch_bounds__(kThreads, 3) leaf3_kernel(const LeafParams<double> p,
+                                                           const double* __restrict__ P) {
+  extern __shared__ __align__(128) double smem3[];
+  double* panel = smem3;                       // nb x 32 right-hand sides (swizzled rows)
+  double* cbuf = smem3 + kLeafMax * kNC;       // TRSM: -(b_I - sum L'X) of the current row block
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = p.n;
+  const int nblk = (n + kRB - 1) / kRB;
+  const int rows_p = nblk * kRB;
+  const i64 c0 = static_cast<i64>(blockIdx.x) * kNC;
+  const int ncols = static_cast<int>(min(static_cast<i64>(kNC), p.nrhs - c0));
+  const bool trsm = p.trsm != 0;
+  constexpr int kWarps = kThreads / 32;
+
+  const i64 rstep = p.reflected ? -1 : 1;
+  auto for_panel = [&](auto&& f) {
+    if (!p.right) {
+      const int rl = lane & 3, cl = lane >> 2;
+#pragma unroll
+      for (int cg = 0; cg < kNC / 8; ++cg) {
+        const int c = 8 * cg + cl;
+        const double* colp = p.B + (c0 + c) * p.ldb + (p.reflected ? n - 1 : 0);
+        for (int rt = warp; rt < rows_p / 4; rt += kWarps) {
+          const int r = 4 * rt + rl;
+          f(r, c, colp + r * rstep);
+        }
+      }
+    } else {
+      const int c = lane;
+      for (int r = warp; r < rows_p; r += kWarps) {
+        const i64 sr = p.reflected ? n - 1 - r : r;
+        f(r, c, p.B + sr * p.ldb + c0 + c);
+      }
+    }
+  };
+
+  if (!trsm && p.alpha == 0.0) {  // base_kernels.cpp:143-150
+    for_panel([&](int r, int c, const double* g) {
+      if (r < n && c < ncols) *const_cast<double*>(g) = 0.0;
+    });
+    return;
+  }
+  for_panel([&](int r, int c, const double* g) {
+    const bool ok = r < n && c < ncols;
+    cp_async8(panel + panel_idx(r, c), ok ? g : p.B, ok ? 8 : 0);
+  });
+  cp_async_commit();
+
+  // warp w owns the m8n8 tiles (w & 3, 2*(w >> 2) + e), e = 0, 1.
+  const int g = lane >> 2, t = lane & 3;
+  const int mt = warp & 3, nt0 = 2 * (warp >> 2);
+  const uint32_t panel_u32 = smem_u32(panel), cbuf_u32 = smem_u32(cbuf);
+  uint32_t b_base[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) b_base[e] = 8u * static_cast<uint32_t>(swz64(t, 8 * (nt0 + e) + g, kNC));
+  const double* pa_base = P + (mt * 32 + lane) * 8;
+  const int nseq = nblk * (nblk + 1) / 2;
+  double nxt[8];
+  auto fetch = [&](int sblk) {
+    const double2* src = reinterpret_cast<const double2*>(pa_base + static_cast<size_t>(sblk) * kBlk);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 v = __ldg(src + q);
+      nxt[2 * q] = v.x;
+      nxt[2 * q + 1] = v.y;
+    }
+  };
+  fetch(0);
+  cp_async_wait<0>();
+  __syncthreads();
+  if (trsm && p.alpha != 1.0) {  // x = alpha * b (base_kernels.cpp:76-77)
+    for_panel([&](int r, int c, const double*) { panel[panel_idx(r, c)] *= p.alpha; });
+    __syncthreads();
+  }
+
+  // c[e][h] += A(block s) * Bsrc(32 rows at byte offset bsrc of a row-major
+  // [k][kNC] swizzled buffer)
+  double c[2][2];
+  int s = 0;
+  auto block_mma = [&](uint32_t bsrc) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = nxt[k];
+    if (s + 1 < nseq) fetch(s + 1);
+    ++s;
+    double bv[2][2];
+    auto ldb = [&](int buf, int kk) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(bv[buf][e]) : "r"(bsrc + b_base[e] + kk * 4 * kNC * 8));
+    };
+    ldb(0, 0);
+#pragma unroll
+    for (int kk = 0; kk < kRB / 4; ++kk) {
+      if (kk + 1 < kRB / 4) ldb((kk + 1) & 1, kk + 1);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) dmma884(c[e][0], c[e][1], a[kk], bv[kk & 1][e]);
+    }
+  };
+
+  for (int bi = 0; bi < nblk; ++bi) {
+    const int I = trsm ? bi : nblk - 1 - bi;
+    const int r0 = I * kRB;
+    if (trsm) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) c[e][h] = -panel[panel_idx(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)];
+    } else {
+      c[0][0] = c[0][1] = c[1][0] = c[1][1] = 0.0;
+    }
+    for (int J = 0; J < I; ++J) block_mma(panel_u32 + static_cast<uint32_t>(J * kRB * kNC * 8));
+    if (trsm) {
+      // c = -(b_I - sum L'X); X_I = (-inv(L'_II)) * c
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) cbuf[panel_idx(8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
+      __syncthreads();
+      c[0][0] = c[0][1] = c[1][0] = c[1][1] = 0.0;
+      block_mma(cbuf_u32);
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) panel[panel_idx(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
+      __syncthreads();  // X_I visible; cbuf free
+    } else {
+      // c += L'_II * b_I; every warp reads b_I before anyone overwrites it
+      block_mma(panel_u32 + static_cast<uint32_t>(I * kRB * kNC * 8));
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          panel[panel_idx(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = p.alpha * c[e][h];
+    }
+  }
+  __syncthreads();
+  for_panel([&](int r, int cc, const double* gp) {
+    if (r < n && cc < ncols) *const_cast<double*>(gp) = panel[panel_idx(r, cc)];
+  });
+}
+
+}  // namespace leaf64v3
+
+size_t leaf3_scratch_doubles() { return leaf64v3::kScratchDoubles; }
+
+void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream_t s) {
+  using namespace leaf64v3;
+  const int nblk = (p.n + kRB - 1) / kRB;
+  if (p.trsm || p.alpha != 0.0) {
+    pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, scratch);
+    ++launch_counter();
+  }
+  const unsigned grid = static_cast<unsigned>(ceil_div(p.nrhs, kNC));
+  cudaFuncSetAttribute(leaf3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  leaf3_kernel<<<grid, kThreads, kSmem, s>>>(p, scratch);
+  ++launch_counter();
+}
+
+}  // namespace rectri_cu

@@ -1,7 +1,8 @@
-"""fp64 leaf kernel v2 (leaf64.cu: packed triangle, bulk-copy ring, solver
-warp) against leaf v1 (leaf.cu) -- identical per-element arithmetic, so the
-two must agree bit for bit on every variant, tile order, right-hand-side
-count and alpha; plus the oracle tolerance and the masking rules."""
+"""fp64 leaf kernels: v2 (leaf64.cu: packed triangle, solver warps) against
+v1 (leaf.cu) -- identical per-element arithmetic, so bit for bit on every
+variant, tile order, right-hand-side count and alpha; v3 (leaf64_v3.cu, the
+default: diagonal blocks as DMMA products with explicit inverses) against
+the oracle tolerance and v1 to rounding; plus the masking rules for each."""
 import itertools
 
 import numpy as np
@@ -42,6 +43,10 @@ def test_leaf_v2_bitwise_equals_v1(cuda, monkeypatch, op, side, uplo, trans, dia
         assert oracle.bitwise_equal(v1, v2), (op, side, uplo, trans, diag, n, m, alpha)
         if n <= 100:
             check_against_oracle(op, s, a, b, v2)
+        v3 = _base(op, s, a, b, 3, monkeypatch)
+        check_against_oracle(op, s, a, b, v3)
+        scale = max(1.0, float(np.max(np.abs(v1))))
+        assert float(np.max(np.abs(v3 - v1))) <= 64 * n * np.finfo(np.float64).eps * scale
 
 
 @pytest.mark.parametrize("op", ["trsm", "trmm"])
@@ -54,28 +59,31 @@ def test_leaf_v2_in_captured_recursion(cuda, monkeypatch, op):
     a, b = _inputs(op, s, n, m, rng)
     fn = rec_trmm if op == "trmm" else rec_trsm
     outs = []
-    for version, be in ((1, Backend.cuda(flags=NO_GRAPH)), (2, Backend.cuda())):
+    for version, be in ((1, Backend.cuda(flags=NO_GRAPH)), (2, Backend.cuda()), (3, Backend.cuda())):
         monkeypatch.setenv("RECTRI_CU_LEAF", str(version))
         A, B = to_dev(a), to_dev(b)
         fn(tspec(s), A.cview(), B.view(), Threshold(256), be)
         outs.append(to_np(B))
     assert oracle.bitwise_equal(outs[0], outs[1])
+    check_against_oracle(op, s, a, b, outs[2]) if n <= 1024 else None
 
 
-def test_leaf_v2_masking_and_alpha_zero(cuda, monkeypatch):
+@pytest.mark.parametrize("version", [2, 3])
+def test_leaf_masking_and_alpha_zero(cuda, monkeypatch, version):
     rng = np.random.default_rng(3)
     n, m = 100, 40
-    for uplo in (0, 1):
-        s = oracle.spec(0, uplo, 0, 1, 1.0)  # Unit: the stored diagonal is never read
-        a, b = _inputs("trsm", s, n, m, rng)
-        junk = a.copy()
-        iu = np.triu_indices(n, 1) if uplo == 0 else np.tril_indices(n, -1)
-        junk[iu] = np.nan
-        np.fill_diagonal(junk, np.nan)
-        ref = _base("trsm", s, a, b, 2, monkeypatch)
-        got = _base("trsm", s, junk, b, 2, monkeypatch)
-        assert np.all(np.isfinite(got)) and oracle.bitwise_equal(ref, got)
+    for op in ("trsm", "trmm"):
+        for uplo in (0, 1):
+            s = oracle.spec(0, uplo, 0, 1, 1.0)  # Unit: the stored diagonal is never read
+            a, b = _inputs(op, s, n, m, rng)
+            junk = a.copy()
+            iu = np.triu_indices(n, 1) if uplo == 0 else np.tril_indices(n, -1)
+            junk[iu] = np.nan
+            np.fill_diagonal(junk, np.nan)
+            ref = _base(op, s, a, b, version, monkeypatch)
+            got = _base(op, s, junk, b, version, monkeypatch)
+            assert np.all(np.isfinite(got)) and oracle.bitwise_equal(ref, got)
     s = oracle.spec(0, 0, 0, 0, 0.0)
     b = F(np.full((n, m), np.nan))
-    got = _base("trmm", s, F(rng.uniform(-1, 1, (n, n))), b, 2, monkeypatch)
+    got = _base("trmm", s, F(rng.uniform(-1, 1, (n, n))), b, version, monkeypatch)
     assert np.all(got == 0.0)

@@ -23,7 +23,7 @@ def _san(tool, args, env_extra=None):
 
 
 @pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
-@pytest.mark.parametrize("args", [["leaf", "100", "70"], ["trmmleaf", "100", "70"], ["gemm", "130", "70", "50"],
+@pytest.mark.parametrize("args", [["leaf", "100", "70"], ["trmmleaf", "100", "70"], ["gemm", "130", "70", "50"], ["gemm", "200", "130", "1100"],
                                   ["trsm", "300", "40", "64"]])
 def test_kernels_clean(cuda, tool, args):
     r = _san(tool, args)
