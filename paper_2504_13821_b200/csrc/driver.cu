@@ -278,7 +278,8 @@ void enqueue_gemm(T alpha, bool ta, DView<const T> A, bool tb, DView<const T> B,
 // validation and the zero-pivot scan).  Tiles above kLeafMax are solved by an
 // internal recursion with the same schema (no events: semantically one call).
 template <typename T>
-void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s);
+void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s,
+                  double* packed = nullptr);
 
 // One kernel of the recursion, as emitted by a descriptor run (the streamed
 // host path executes these itself).
@@ -305,6 +306,11 @@ class Recursion {
   std::function<void(bool leaf, DView<const T> a, DView<T> b1, DView<T> b2)> before;
   // Descriptor mode: every kernel is handed to `kernels` instead of launched.
   std::function<void(const KDesc<T>&)> kernels;
+  // fp64 leaves whose triangles were packed once for the whole call
+  // (launch_leaf3_pack_all): leaf k reads packed + k * packed_stride.
+  double* packed = nullptr;
+  size_t packed_stride = 0;
+  int leaf_idx = 0;
 
   // recursion.cpp:85-148
   void run(const Spec& spec, DView<const T> A, DView<T> B, i64 row0) {
@@ -315,7 +321,8 @@ class Recursion {
       if (leaves_) leaves_->push_back({row0, n});
       if (before) before(true, A, B, B);
       if (kernels) kernels(KDesc<T>{true, spec, A, B, B, T(0), false, false});
-      else if (!dry_) enqueue_base<T>(op_, spec, A, B, s_);
+      else if (!dry_) enqueue_base<T>(op_, spec, A, B, s_, packed ? packed + leaf_idx * packed_stride : nullptr);
+      ++leaf_idx;
       return;
     }
     const i64 mid = n / 2;  // split_half
@@ -360,8 +367,29 @@ class Recursion {
   bool dry_;
 };
 
+// The leaf problem of a base call in the Left form on L' (base_kernels.cpp:35-47, 152-155).
 template <typename T>
-void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s) {
+LeafParams<T> leaf_params(OpK op, const Spec& spec, DView<const T> A, DView<T> B) {
+  const bool left = spec.side == RECTRI_CU_LEFT;
+  const int eff = left ? spec.trans : 1 - spec.trans;
+  LeafParams<T> p;
+  p.n = static_cast<int>(A.rows);
+  p.nrhs = left ? B.cols : B.rows;
+  p.A = A.p;
+  p.lda = A.ld;
+  p.B = B.p;
+  p.ldb = B.ld;
+  p.right = left ? 0 : 1;
+  p.reflected = (spec.uplo == RECTRI_CU_LOWER) == (eff == 1) ? 1 : 0;
+  p.swapped = eff == 1 ? 1 : 0;
+  p.unit = spec.diag == RECTRI_CU_UNIT ? 1 : 0;
+  p.trsm = op == kTrsm ? 1 : 0;
+  p.alpha = static_cast<T>(spec.alpha);
+  return p;
+}
+
+template <typename T>
+void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s, double* packed) {
   const i64 n = A.rows;
   const bool left = spec.side == RECTRI_CU_LEFT;
   const i64 rhs = left ? B.cols : B.rows;
@@ -385,6 +413,7 @@ void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaSt
   p.unit = spec.diag == RECTRI_CU_UNIT ? 1 : 0;
   p.trsm = op == kTrsm ? 1 : 0;
   p.alpha = static_cast<T>(spec.alpha);
+  if constexpr (std::is_same<T, double>::value) p.packed = packed;
   ProfScope prof(1, static_cast<double>(n) * n * rhs, s);
   K<T>::leaf(p, s);
 }
@@ -444,10 +473,14 @@ struct GraphEntry {
   std::vector<std::pair<i64, i64>> leaves;
   uint8_t* d_flags = nullptr;
   uint8_t* h_flags = nullptr;
+  double* packed = nullptr;  // fp64 leaf triangles, packed once per call
+  void* leaf_meta = nullptr;  // their row offsets and orders
   i64 nodes = 0;
   int device = 0;
   ~GraphEntry() {
     if (exec) cudaGraphExecDestroy(exec);
+    if (packed) cudaFree(packed);
+    if (leaf_meta) cudaFree(leaf_meta);
     if (d_flags) cudaFree(d_flags);
     if (h_flags) cudaFreeHost(h_flags);
   }
@@ -518,6 +551,42 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
     cuda_check(cudaMallocHost(&g->h_flags, static_cast<size_t>(A.rows)), "flags alloc");
   }
   Spec eff = spec;
+  if (op == kTrsm) eff.alpha = 1.0;
+  // fp64 v3 leaves: pack every leaf's triangle once, up front, for all
+  // right-hand-side streams (allocations before any capture).
+  LeafParams<double> pbase{};
+  int nleaves = 0;
+  if constexpr (std::is_same<T, double>::value) {
+    if (leaf_version() >= 3 && threshold <= kLeafMax && !(op == kTrmm && spec.alpha == 0.0)) {
+      std::vector<std::pair<i64, i64>> lv;
+      Recursion<T>(op, threshold, nullptr, nullptr, &lv, true).run(eff, A, B, 0);
+      nleaves = static_cast<int>(lv.size());
+      std::vector<long long> r0s(nleaves);
+      std::vector<int> ns(nleaves);
+      for (int k = 0; k < nleaves; ++k) {
+        r0s[k] = lv[k].first;
+        ns[k] = static_cast<int>(lv[k].second);
+      }
+      cuda_check(cudaMalloc(&g->packed, static_cast<size_t>(nleaves) * leaf3_scratch_doubles() * sizeof(double)),
+                 "leaf pack alloc");
+      cuda_check(cudaMalloc(&g->leaf_meta, static_cast<size_t>(nleaves) * (sizeof(long long) + sizeof(int))),
+                 "leaf meta alloc");
+      long long* d_r0 = static_cast<long long*>(g->leaf_meta);
+      int* d_n = reinterpret_cast<int*>(d_r0 + nleaves);
+      cuda_check(cudaMemcpy(d_r0, r0s.data(), nleaves * sizeof(long long), cudaMemcpyHostToDevice), "leaf meta");
+      cuda_check(cudaMemcpy(d_n, ns.data(), nleaves * sizeof(int), cudaMemcpyHostToDevice), "leaf meta");
+      const bool left = spec.side == RECTRI_CU_LEFT;
+      const int effop = left ? spec.trans : 1 - spec.trans;
+      pbase.A = A.p;
+      pbase.lda = A.ld;
+      pbase.right = left ? 0 : 1;
+      pbase.reflected = (spec.uplo == RECTRI_CU_LOWER) == (effop == 1) ? 1 : 0;
+      pbase.swapped = effop == 1 ? 1 : 0;
+      pbase.unit = spec.diag == RECTRI_CU_UNIT ? 1 : 0;
+      pbase.trsm = op == kTrsm ? 1 : 0;
+      pbase.alpha = eff.alpha;
+    }
+  }
   i64& counter = launch_counter();
   const i64 before = counter;
   if (capture) {
@@ -527,13 +596,21 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
     for (cudaStream_t a : res.aux) leaf_scratch_reserve(a);
     cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
   }
-  if (op == kTrsm) {
-    if (spec.alpha != 1.0) {
-      ProfScope prof(2, 0.0, s);
-      K<T>::scale(B.p, B.ld, B.rows, B.cols, static_cast<T>(spec.alpha), s);
-    }
-    eff.alpha = 1.0;
+  if (op == kTrsm && spec.alpha != 1.0) {
+    ProfScope prof(2, 0.0, s);
+    K<T>::scale(B.p, B.ld, B.rows, B.cols, static_cast<T>(spec.alpha), s);
   }
+  if (nleaves > 0) {
+    long long* d_r0 = static_cast<long long*>(g->leaf_meta);
+    launch_leaf3_pack_all(pbase, d_r0, reinterpret_cast<int*>(d_r0 + nleaves), nleaves, g->packed, s);
+  }
+  auto with_packs = [&](Recursion<T>& r) -> Recursion<T>& {
+    if (nleaves > 0) {
+      r.packed = g->packed;
+      r.packed_stride = leaf3_scratch_doubles();
+    }
+    return r;
+  };
   if (scan) {
     ProfScope prof(3, 0.0, s);
     K<T>::scan(A.p, A.ld, A.rows, g->d_flags, s);
@@ -543,7 +620,8 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
   const i64 rhs = left ? B.cols : B.rows;
   const int P = g_prof.on ? 1 : panel_streams(rhs);
   if (P <= 1) {
-    Recursion<T>(op, threshold, s, &g->events, &g->leaves).run(eff, A, B, 0);
+    Recursion<T> rec(op, threshold, s, &g->events, &g->leaves);
+    with_packs(rec).run(eff, A, B, 0);
   } else {
     // Right-hand-side panels on P streams (fork/join inside the capture):
     // one panel's small kernels (leaves, short-K GEMMs) fill the SMs another
@@ -576,7 +654,8 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
       const DView<T> panel = left ? B.sub(0, r0, B.rows, wi) : B.sub(r0, 0, wi, B.cols);
       cudaStream_t sk = k == 0 ? s : res.aux[k - 1];
       if (k > 0) cuda_check(cudaStreamWaitEvent(sk, fork, 0), "wait fork");
-      Recursion<T>(op, threshold, sk, nullptr, nullptr).run(eff, A, panel, 0);
+      Recursion<T> rec(op, threshold, sk, nullptr, nullptr);
+      with_packs(rec).run(eff, A, panel, 0);
       if (k > 0) {
         cudaEvent_t join = ev();
         cuda_check(cudaEventRecord(join, sk), "record join");
@@ -968,12 +1047,33 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
       const i64 r0 = q * pw, r1 = std::min(rhs, r0 + pw);
       return left ? v.sub(0, r0, v.rows, r1 - r0) : v.sub(r0, 0, r1 - r0, v.cols);
     };
+    // fp64 v3 leaves: each leaf's triangle packed once (stream 0, after its
+    // A block has arrived), shared by every stream's leaf launch.
+    double* packs = nullptr;
+    const bool pack_once = std::is_same<T, double>::value && leaf_version() >= 3 && threshold <= kLeafMax &&
+                           !(op == kTrmm && spec.alpha == 0.0) && P > 1;
+    if (pack_once) {
+      std::lock_guard<std::mutex> lock(g_mu);
+      packs = static_cast<double*>(staging(*res, 2, leaves.size() * leaf3_scratch_doubles() * sizeof(double)));
+    }
+    int leaf_k = 0;
     for (size_t i = 0; i < units.size(); ++i) {
       const Unit& u = units[i];
       const KDesc<T>& k = *u.k;
+      double* packed = nullptr;
+      cudaEvent_t packed_ev = nullptr;
+      if (pack_once && k.leaf) {
+        if (ready[i]) cuda_check(cudaStreamWaitEvent(ps[0], ready[i], 0), "wait input");
+        packed = packs + static_cast<size_t>(leaf_k++) * leaf3_scratch_doubles();
+        if constexpr (std::is_same<T, double>::value)
+          launch_leaf3_pack(leaf_params<double>(op, k.spec, k.a, k.dst), packed, ps[0]);
+        packed_ev = ev();
+        cuda_check(cudaEventRecord(packed_ev, ps[0]), "record");
+      }
       for (int q = 0; q < P && q * pw < rhs; ++q) {
         cudaStream_t sq = ps[q];
         if (ready[i]) cuda_check(cudaStreamWaitEvent(sq, ready[i], 0), "wait input");
+        if (packed_ev && q > 0) cuda_check(cudaStreamWaitEvent(sq, packed_ev, 0), "wait pack");
         if (op == kTrsm && spec.alpha != 1.0)  // alpha once per element, at first arrival
           for (int c : fresh[i]) {
             const DView<T> d = rhs_part(b_chunk(dB, c), q);
@@ -981,7 +1081,7 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
           }
         const DView<T> dst = rhs_part(u.dst, q);
         if (k.leaf) {
-          enqueue_base<T>(op, k.spec, k.a, dst, sq);
+          enqueue_base<T>(op, k.spec, k.a, dst, sq, packed);
         } else if (k.off_on_left) {
           enqueue_gemm<T>(k.coeff, k.off_trans, u.a, false, rhs_part(k.src, q), T(1), dst, sq);
         } else {

@@ -47,6 +47,7 @@ struct LeafParams {
   // part (timing), 3 planted missing barrier (racecheck negative test).
   int debug_skip = 0;
   long long* trace = nullptr;  // RECTRI_CU_LEAF_TRACE: per-CTA clock64 stamps (leaf64.cu)
+  double* packed = nullptr;    // v3: this leaf's triangle already packed here (pack3_all_kernel)
 };
 
 constexpr int kLeafMax = 256;
@@ -55,7 +56,17 @@ void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t
 void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s);
 void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s);     // leaf64.cu (v2)
 void launch_leaf_f64_v1(const LeafParams<double>& p, cudaStream_t s);  // leaf.cu
-void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream_t s);  // leaf64_v3.cu
+void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream_t s,
+                        bool prepacked = false);  // leaf64_v3.cu
+// Packs the triangles of all leaves of one recursion (leaf k: order d_n[k]
+// at A(d_r0[k], d_r0[k]); base carries A, lda and the variant flags) into
+// scratch + k * leaf3_scratch_doubles().
+void launch_leaf3_pack_all(const LeafParams<double>& base, const long long* d_r0, const int* d_n, int nleaves,
+                           double* scratch, cudaStream_t s);
+size_t leaf3_scratch_doubles();
+// Packs one leaf's triangle (p.A, p.n, variant flags) into dst.
+void launch_leaf3_pack(const LeafParams<double>& p, double* dst, cudaStream_t s);
+int leaf_version();  // RECTRI_CU_LEAF (fp64: 1 = leaf.cu, 2 = leaf64.cu, 3 = leaf64_v3.cu)
 // Allocates the v2 fp64 leaf's per-stream scratch (call before capturing on s).
 void leaf_scratch_reserve(cudaStream_t s);
 void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s);

@@ -302,20 +302,18 @@ __global__ void __launch_bounds__(kThreads, 2) leaf64_kernel(const LeafParams<do
           if (tid == 0) stamp(2 + 4 * bi + 3);
         }
         const uint32_t pb = panel_u32 + static_cast<uint32_t>(J * kRB * kNC * 8);
-        double bv[2][2];
-        auto ldb = [&](int buf, int kk) {
+        if (p.debug_skip == 2) continue;  // timing experiment: no GEMM part
+        // all 8 k-steps' B fragments first: one shared-memory latency per block
+        double bv[kRB / 4][2];
+#pragma unroll
+        for (int kk = 0; kk < kRB / 4; ++kk)
 #pragma unroll
           for (int e = 0; e < 2; ++e)
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(bv[buf][e]) : "r"(pb + b_base[e] + kk * 4 * kNC * 8));
-        };
-        if (p.debug_skip == 2) continue;  // timing experiment: no GEMM part
-        ldb(0, 0);
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(bv[kk][e]) : "r"(pb + b_base[e] + kk * 4 * kNC * 8));
 #pragma unroll
-        for (int kk = 0; kk < kRB / 4; ++kk) {
-          if (kk + 1 < kRB / 4) ldb((kk + 1) & 1, kk + 1);
+        for (int kk = 0; kk < kRB / 4; ++kk)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) dmma884(c[e][0], c[e][1], a[kk], bv[kk & 1][e]);
-        }
+          for (int e = 0; e < 2; ++e) dmma884(c[e][0], c[e][1], a[kk], bv[kk][e]);
       }
       if (trsm) {
         // b' = b - sum L'x into the panel rows of block I (the solver's input)
@@ -451,22 +449,29 @@ double* scratch_for(cudaStream_t s, bool may_alloc) {
   return ptr;
 }
 
-int leaf_version() {
-  // 2 (default): substitution in the reference's order, bitwise equal to v1;
-  // 3: explicit-inverse diagonal blocks (leaf64_v3.cu), ~15 % faster leaves.
+int leaf_version_env() {
+  // 3 (default): explicit-inverse diagonal blocks as DMMA products
+  // (leaf64_v3.cu), ~2x faster leaves; 2: warp-shuffle substitution in the
+  // reference's order, bitwise equal to v1 (leaf.cu).
   const char* e = getenv("RECTRI_CU_LEAF");
-  return e ? atoi(e) : 2;
+  return e ? atoi(e) : 3;
 }
 
 }  // namespace leaf64
+
+int leaf_version() { return leaf64::leaf_version_env(); }
 
 void leaf_scratch_reserve(cudaStream_t s) { leaf64::scratch_for(s, true); }
 
 void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s) {
   using namespace leaf64;
   if (p.n <= 0 || p.nrhs <= 0) return;
+  if (p.packed) {  // triangle packed once for the whole recursion
+    launch_leaf_f64_v3(p, p.packed, s, true);
+    return;
+  }
   double* P = nullptr;
-  if (leaf_version() >= 2) {
+  if (leaf64::leaf_version_env() >= 2) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cs);
     P = scratch_for(s, cs == cudaStreamCaptureStatusNone);
@@ -475,7 +480,7 @@ void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s) {
     launch_leaf_f64_v1(p, s);
     return;
   }
-  if (leaf_version() >= 3) {
+  if (leaf64::leaf_version_env() >= 3) {
     launch_leaf_f64_v3(p, P, s);
     return;
   }

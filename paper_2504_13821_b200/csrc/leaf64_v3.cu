@@ -53,10 +53,12 @@ __device__ __forceinline__ double lprime(const LeafParams<double>& p, int r, int
   return p.A[row + col * p.lda];
 }
 
-// Fragment order position of element (r, k) of a 32x32 block.
+// Fragment order position of element (r, k) of a 32x32 block: [row tile
+// mt][k-step kk][lane], so a warp's 8-byte fragment reads of one k-step are
+// 256 contiguous bytes in shared memory (conflict-free).
 __device__ __forceinline__ int frag_pos(int r, int k) {
   const int mt = r >> 3, g = r & 7, kk = k >> 2, t = k & 3;
-  return (mt * 32 + 4 * g + t) * 8 + kk;
+  return (mt * 8 + kk) * 32 + 4 * g + t;
 }
 
 // Consumption index of block (I, J) (J == I: the diagonal block).
@@ -66,12 +68,11 @@ __device__ __forceinline__ int seq_of(int I, int J, int nblk, bool asc) {
   return (nblk * (nblk + 1) / 2 - (I + 1) * (I + 2) / 2) + J;
 }
 
-__global__ void __launch_bounds__(256) pack3_kernel(const LeafParams<double> p, double* __restrict__ P) {
+__device__ void pack3_block(const LeafParams<double>& p, double* __restrict__ P, const int b) {
   __shared__ double L[kRB][kRB + 1];
   const int nblk = (p.n + kRB - 1) / kRB;
   const bool trsm = p.trsm != 0;
-  // blockIdx.x -> (I, J), J <= I, canonical ascending numbering
-  const int b = blockIdx.x;
+  // b -> (I, J), J <= I, canonical ascending numbering
   int I = 0;
   while ((I + 1) * (I + 2) / 2 <= b) ++I;
   const int J = b - I * (I + 1) / 2;
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(256) pack3_kernel(const LeafParams<double> p, 
   const int tid = threadIdx.x;
   if (J < I) {
     for (int o = tid; o < kBlk; o += blockDim.x) {
-      const int kk = o & 7, ln = (o >> 3) & 31, mt = o >> 8;
+      const int ln = o & 31, kk = (o >> 5) & 7, mt = o >> 8;
       const int r = 8 * mt + (ln >> 2), k = 4 * kk + (ln & 3);
       dst[o] = r0 + r < p.n ? lprime(p, r0 + r, j0 + k) : 0.0;
     }
@@ -121,13 +122,65 @@ __global__ void __launch_bounds__(256) pack3_kernel(const LeafParams<double> p, 
   }
 }
 
-constexpr int kSmem = (kLeafMax * kNC + kRB * kNC) * 8;
+__global__ void __launch_bounds__(256) pack3_kernel(const LeafParams<double> p, double* __restrict__ P) {
+  pack3_block(p, P, blockIdx.x);
+}
 
-__global__ void __launch_bounds__(kThreads, 3) leaf3_kernel(const LeafParams<double> p,
-                                                           const double* __restrict__ P) {
+// Every leaf of one recursion at once (blockIdx.y = leaf): leaf k's tile is
+// A(r0_k.., r0_k..) of order n_k, packed into P + k * stride.
+__global__ void __launch_bounds__(256) pack3_all_kernel(const LeafParams<double> base, const long long* __restrict__ r0s,
+                                                        const int* __restrict__ ns, double* __restrict__ P,
+                                                        long long stride) {
+  const int k = blockIdx.y;
+  LeafParams<double> p = base;
+  p.n = ns[k];
+  p.A = base.A + r0s[k] * (1 + base.lda);
+  const int nblk = (p.n + kRB - 1) / kRB;
+  if (static_cast<int>(blockIdx.x) >= nblk * (nblk + 1) / 2) return;
+  pack3_block(p, P + static_cast<size_t>(k) * stride, blockIdx.x);
+}
+
+constexpr int kRing = 5;  // packed blocks in flight (bulk copies)
+constexpr int kSmem = (kLeafMax * kNC + kRB * kNC + kRing * kBlk) * 8 + 2 * kRing * 8;
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParams<double> p,
+                                                                const double* __restrict__ P) {
   extern __shared__ __align__(128) double smem3[];
   double* panel = smem3;                       // nb x 32 right-hand sides (swizzled rows)
   double* cbuf = smem3 + kLeafMax * kNC;       // TRSM: -(b_I - sum L'X) of the current row block
+  double* ring = cbuf + kRB * kNC;             // kRing packed blocks
+  const uint32_t full0 = smem_u32(ring + kRing * kBlk), empty0 = full0 + 8 * kRing;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = p.n;
   const int nblk = (n + kRB - 1) / kRB;
@@ -160,9 +213,30 @@ __global__ void __launch_bounds__(kThreads, 3) leaf3_kernel(const LeafParams<dou
   };
 
   if (!trsm && p.alpha == 0.0) {  // base_kernels.cpp:143-150
-    for_panel([&](int r, int c, const double* g) {
-      if (r < n && c < ncols) *const_cast<double*>(g) = 0.0;
-    });
+    if (warp < kWarps)
+      for_panel([&](int r, int c, const double* g) {
+        if (r < n && c < ncols) *const_cast<double*>(g) = 0.0;
+      });
+    return;
+  }
+  const int nseq = nblk * (nblk + 1) / 2;
+  if (tid == 0) {
+    for (int q = 0; q < kRing; ++q) {
+      mbar_init(full0 + 8 * q, 1);
+      mbar_init(empty0 + 8 * q, kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kWarps) {  // producer warp: packed blocks through the ring
+    if (lane == 0)
+      for (int q = 0; q < nseq; ++q) {
+        const int slot = q % kRing;
+        if (q >= kRing) mbar_wait(empty0 + 8 * slot, ((q / kRing) + 1) & 1);
+        mbar_expect_tx(full0 + 8 * slot, kBlk * 8);
+        bulk_g2s(smem_u32(ring + slot * kBlk), P + static_cast<size_t>(q) * kBlk, kBlk * 8, full0 + 8 * slot);
+      }
     return;
   }
   for_panel([&](int r, int c, const double* g) {
@@ -178,24 +252,12 @@ __global__ void __launch_bounds__(kThreads, 3) leaf3_kernel(const LeafParams<dou
   uint32_t b_base[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) b_base[e] = 8u * static_cast<uint32_t>(swz64(t, 8 * (nt0 + e) + g, kNC));
-  const double* pa_base = P + (mt * 32 + lane) * 8;
-  const int nseq = nblk * (nblk + 1) / 2;
-  double nxt[8];
-  auto fetch = [&](int sblk) {
-    const double2* src = reinterpret_cast<const double2*>(pa_base + static_cast<size_t>(sblk) * kBlk);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double2 v = __ldg(src + q);
-      nxt[2 * q] = v.x;
-      nxt[2 * q + 1] = v.y;
-    }
-  };
-  fetch(0);
+  const uint32_t a_off = static_cast<uint32_t>((mt * 8 * 32 + lane) * 8);  // this lane's k-step-0 A fragment
   cp_async_wait<0>();
-  __syncthreads();
+  named_sync(1, kThreads);  // panel loaded (GEMM warps only; the producer runs free)
   if (trsm && p.alpha != 1.0) {  // x = alpha * b (base_kernels.cpp:76-77)
     for_panel([&](int r, int c, const double*) { panel[panel_idx(r, c)] *= p.alpha; });
-    __syncthreads();
+    named_sync(1, kThreads);
   }
 
   // c[e][h] += A(block s) * Bsrc(32 rows at byte offset bsrc of a row-major
@@ -203,24 +265,30 @@ __global__ void __launch_bounds__(kThreads, 3) leaf3_kernel(const LeafParams<dou
   double c[2][2];
   int s = 0;
   auto block_mma = [&](uint32_t bsrc) {
+    const int slot = s % kRing;
+    mbar_wait(full0 + 8 * slot, (s / kRing) & 1);
+    const uint32_t as = smem_u32(ring + slot * kBlk) + a_off;
     double a[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = nxt[k];
-    if (s + 1 < nseq) fetch(s + 1);
-    ++s;
-    double bv[2][2];
-    auto ldb = [&](int buf, int kk) {
+    for (int kk = 0; kk < 8; ++kk)
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[kk]) : "r"(as + kk * 32 * 8));
+    // all 8 k-steps' B fragments first: one shared-memory latency per block
+    double bv[kRB / 4][2];
+#pragma unroll
+    for (int kk = 0; kk < kRB / 4; ++kk)
 #pragma unroll
       for (int e = 0; e < 2; ++e)
-        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(bv[buf][e]) : "r"(bsrc + b_base[e] + kk * 4 * kNC * 8));
-    };
-    ldb(0, 0);
-#pragma unroll
-    for (int kk = 0; kk < kRB / 4; ++kk) {
-      if (kk + 1 < kRB / 4) ldb((kk + 1) & 1, kk + 1);
-#pragma unroll
-      for (int e = 0; e < 2; ++e) dmma884(c[e][0], c[e][1], a[kk], bv[kk & 1][e]);
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(bv[kk][e]) : "r"(bsrc + b_base[e] + kk * 4 * kNC * 8));
+    __syncwarp();
+    if (lane == 0) {  // fragments are in registers: release the slot to the async (bulk-copy) proxy
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive(empty0 + 8 * slot);
     }
+    ++s;
+#pragma unroll
+    for (int kk = 0; kk < kRB / 4; ++kk)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) dmma884(c[e][0], c[e][1], a[kk], bv[kk][e]);
   };
 
   for (int bi = 0; bi < nblk; ++bi) {
@@ -241,18 +309,18 @@ __global__ void __launch_bounds__(kThreads, 3) leaf3_kernel(const LeafParams<dou
       for (int e = 0; e < 2; ++e)
 #pragma unroll
         for (int h = 0; h < 2; ++h) cbuf[panel_idx(8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
-      __syncthreads();
+      named_sync(1, kThreads);
       c[0][0] = c[0][1] = c[1][0] = c[1][1] = 0.0;
       block_mma(cbuf_u32);
 #pragma unroll
       for (int e = 0; e < 2; ++e)
 #pragma unroll
         for (int h = 0; h < 2; ++h) panel[panel_idx(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
-      __syncthreads();  // X_I visible; cbuf free
+      named_sync(1, kThreads);  // X_I visible; cbuf free
     } else {
       // c += L'_II * b_I; every warp reads b_I before anyone overwrites it
       block_mma(panel_u32 + static_cast<uint32_t>(I * kRB * kNC * 8));
-      __syncthreads();
+      named_sync(1, kThreads);
 #pragma unroll
       for (int e = 0; e < 2; ++e)
 #pragma unroll
@@ -260,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 3) leaf3_kernel(const LeafParams<dou
           panel[panel_idx(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = p.alpha * c[e][h];
     }
   }
-  __syncthreads();
+  named_sync(1, kThreads);
   for_panel([&](int r, int cc, const double* gp) {
     if (r < n && cc < ncols) *const_cast<double*>(gp) = panel[panel_idx(r, cc)];
   });
@@ -270,16 +338,31 @@ __global__ void __launch_bounds__(kThreads, 3) leaf3_kernel(const LeafParams<dou
 
 size_t leaf3_scratch_doubles() { return leaf64v3::kScratchDoubles; }
 
-void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream_t s) {
+void launch_leaf3_pack_all(const LeafParams<double>& base, const long long* d_r0, const int* d_n, int nleaves,
+                           double* scratch, cudaStream_t s) {
+  using namespace leaf64v3;
+  dim3 grid(kMaxBlk * (kMaxBlk + 1) / 2, nleaves);
+  pack3_all_kernel<<<grid, 256, 0, s>>>(base, d_r0, d_n, scratch, static_cast<long long>(kScratchDoubles));
+  ++launch_counter();
+}
+
+void launch_leaf3_pack(const LeafParams<double>& p, double* dst, cudaStream_t s) {
   using namespace leaf64v3;
   const int nblk = (p.n + kRB - 1) / kRB;
-  if (p.trsm || p.alpha != 0.0) {
+  pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, dst);
+  ++launch_counter();
+}
+
+void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream_t s, bool prepacked) {
+  using namespace leaf64v3;
+  const int nblk = (p.n + kRB - 1) / kRB;
+  if (!prepacked && (p.trsm || p.alpha != 0.0)) {
     pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, scratch);
     ++launch_counter();
   }
   const unsigned grid = static_cast<unsigned>(ceil_div(p.nrhs, kNC));
   cudaFuncSetAttribute(leaf3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-  leaf3_kernel<<<grid, kThreads, kSmem, s>>>(p, scratch);
+  leaf3_kernel<<<grid, kThreads + 32, kSmem, s>>>(p, scratch);
   ++launch_counter();
 }
 
