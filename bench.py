@@ -249,7 +249,7 @@ def main():
         return
 
     import paper_2504_13821_b200 as rc
-    from paper_2504_13821_b200 import (ASYNC, Backend, Diag, MatrixBuffer, Side, Threshold, Trans,
+    from paper_2504_13821_b200 import (ASYNC, TF32X3, Backend, Diag, MatrixBuffer, Side, Threshold, Trans,
                                        TriangularSpec, Uplo)
 
     dev = torch.device("cuda", local)
@@ -279,20 +279,20 @@ def main():
     }
     flops_per_gpu = float(n) * n * m
 
-    def one(op, Abuf=None, Bbuf=None):
+    def one(op, Abuf=None, Bbuf=None, backend=None):
         Abuf = Abuf if Abuf is not None else A
         Bbuf = Bbuf if Bbuf is not None else B
         fn = rc.rec_trsm if op == "trsm" else rc.rec_trmm
         if world > 1:
             dist.broadcast(Abuf.data, src=0)
-        fn(specs[op], Abuf.cview(), Bbuf.view(), Threshold(args.threshold), be)
+        fn(specs[op], Abuf.cview(), Bbuf.view(), Threshold(args.threshold), backend or be)
 
-    def timed(op, Abuf=None, Bbuf=None, B0buf=None):
+    def timed(op, Abuf=None, Bbuf=None, B0buf=None, backend=None):
         Bbuf = Bbuf if Bbuf is not None else B
         B0buf = B0buf if B0buf is not None else B0
         for _ in range(args.warmup):
             Bbuf.data.copy_(B0buf.data)
-            one(op, Abuf, Bbuf)
+            one(op, Abuf, Bbuf, backend)
         rc.sync(stream)
         barrier(world)
         launches0 = rc.launch_count()
@@ -303,7 +303,7 @@ def main():
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                one(op, Abuf, Bbuf)
+                one(op, Abuf, Bbuf, backend)
                 e1.record(stream)
                 evs.append((e0, e1))
             rc.sync(stream)
@@ -362,6 +362,25 @@ def main():
             except Exception as e:  # pragma: no cover
                 fp32["cublas_strsm_LLN"] = {"error": str(e)}
         log(f"fp32 trsm: {v32:.1f} GFLOP/s, {ms32:.2f} ms/step")
+        # Opt-in 3xTF32 variant on tcgen05 (csrc/sgemm_tf32x3.cu), reported
+        # separately with its own residual on 8 sampled columns.
+        be_tf = Backend.cuda(device=local, stream=stream, flags=ASYNC | TF32X3)
+        vt, mst, lt, clkt = timed("trsm", A32, B32, B32_0, be_tf)
+        B32.data.copy_(B32_0.data)
+        one("trsm", A32, B32, be_tf)
+        rc.sync(stream)
+        Xt = B32.data[cols].t().double()
+        L32 = torch.tril(A32.data.t().double())
+        Bt = B32_0.data[cols].t().double()
+        res_t = (L32 @ Xt - Bt).abs().max().item()
+        eta_t = res_t / (L32.abs().sum(1).max().item() * max(Xt.abs().max().item(), Bt.abs().max().item(), 1.0)
+                         * n * float(np.finfo(np.float32).eps))
+        del L32, Xt, Bt
+        fp32["tf32x3"] = {"value": vt, "unit": "GFLOP/s", "ms_per_step": mst, "gpu_launches": lt, "clocks": clkt,
+                          "residual_eta_fp32": eta_t, "tolerance": "eta <= 32 (the fp32 criterion of the FFMA path)",
+                          "workload": "same TRSM, fp32 GEMM updates as 3xTF32 (hi/lo split, 3 tcgen05 kind::tf32 "
+                                      "MMAs per k-step, fp32 accumulation in TMEM); opt-in RECTRI_CU_TF32X3"}
+        log(f"fp32 trsm 3xTF32: {vt:.1f} GFLOP/s, {mst:.2f} ms/step, eta {eta_t:.3e}")
         del A32, B32_0, B32
         torch.cuda.empty_cache()
 

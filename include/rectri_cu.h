@@ -87,12 +87,15 @@ typedef struct rectri_cu_view {
 /* backend->flags */
 #define RECTRI_CU_ASYNC 1u    /* do not synchronize before returning        */
 #define RECTRI_CU_NO_GRAPH 2u /* launch kernels directly, no graph capture  */
+#define RECTRI_CU_TF32X3 4u   /* fp32 GEMM updates as 3xTF32 on tcgen05: an
+                                 opt-in variant, reported separately under its
+                                 own tolerance (default fp32 is exact FFMA)    */
 
 typedef struct rectri_cu_backend {
   int32_t parallel_width; /* validated >= 1 (backend.hpp:31-37)            */
   int32_t device;         /* CUDA ordinal; -1 = the current device         */
   void* stream;           /* cudaStream_t; NULL = legacy default stream    */
-  uint32_t flags;         /* RECTRI_CU_ASYNC | RECTRI_CU_NO_GRAPH          */
+  uint32_t flags;         /* RECTRI_CU_ASYNC | RECTRI_CU_NO_GRAPH | RECTRI_CU_TF32X3 */
   int64_t mc, kc, nc;     /* GemmBlocking, validated >= 1 (advisory on GPU) */
 } rectri_cu_backend;
 

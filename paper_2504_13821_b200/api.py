@@ -294,6 +294,7 @@ class GemmBlocking:
 
 ASYNC = 1
 NO_GRAPH = 2
+TF32X3 = 4  # fp32 GEMM updates as 3xTF32 on tcgen05 (opt-in variant, own tolerance)
 
 
 @dataclass

@@ -99,6 +99,12 @@ struct BackendInfo {
   unsigned flags = 0;
 };
 
+// RECTRI_CU_TF32X3 for the duration of one fp32 call on this thread.
+struct Tf32x3Scope {
+  explicit Tf32x3Scope(bool on) { tf32x3_set_call(on); }
+  ~Tf32x3Scope() { tf32x3_set_call(false); }
+};
+
 BackendInfo validate_backend(const rectri_cu_backend* b) {
   BackendInfo out;
   if (!b) return out;  // Backend{} defaults
@@ -594,6 +600,13 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
     DeviceRes& res = device_res(dev);  // the capture path holds g_mu
     leaf_scratch_reserve(s);
     for (cudaStream_t a : res.aux) leaf_scratch_reserve(a);
+    if (std::is_same<T, float>::value && tf32x3_enabled()) {
+      // 3xTF32 operand splits: hi + lo of the largest off-diagonal block and source half
+      const i64 n = A.rows, h = n - n / 2, rhs = spec.side == RECTRI_CU_LEFT ? B.cols : B.rows;
+      const size_t need = 2 * static_cast<size_t>(h * h + h * rhs);
+      tf32x3_reserve(s, need);
+      for (cudaStream_t a : res.aux) tf32x3_reserve(a, need);
+    }
     cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
   }
   if (op == kTrsm && spec.alpha != 1.0) {
@@ -708,7 +721,8 @@ std::shared_ptr<GraphEntry> enqueue_device(OpK op, const Spec& spec, DView<const
       if (sink) sink(user, e.e, e.n, e.m);
     return g;
   }
-  const Key key{static_cast<int>(op), dtype_code<T>(), spec.side, spec.uplo, spec.trans,
+  const int mode = dtype_code<T>() + (std::is_same<T, float>::value && tf32x3_enabled() ? 10 : 0);
+  const Key key{static_cast<int>(op), mode, spec.side, spec.uplo, spec.trans,
                 spec.diag, bits_of(spec.alpha), static_cast<const void*>(A.p), A.ld, A.rows,
                 static_cast<void*>(B.p), B.ld, B.rows, B.cols, threshold, dev};
   {
@@ -1180,6 +1194,7 @@ void rec_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
   // conformal, alias -- in that order.
   const Spec spec = validate_spec(cspec);
   const BackendInfo be = validate_backend(cbe);
+  const Tf32x3Scope tf32x3_scope(std::is_same<T, float>::value && (be.flags & RECTRI_CU_TF32X3));
   if (threshold < 1) fail(RECTRI_CU_CONFIG, "threshold must be >= 1");
   if (Av.rows != Av.cols)
     fail(RECTRI_CU_SHAPE, "triangular A must be square, got %lldx%lld", (long long)Av.rows,
@@ -1287,6 +1302,7 @@ void base_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
          (long long)tile_limit);
   if (overlaps(Av, Bv)) fail(RECTRI_CU_ALIAS, "A and B views overlap");
   const BackendInfo be = validate_backend(cbe);
+  const Tf32x3Scope tf32x3_scope(std::is_same<T, float>::value && (be.flags & RECTRI_CU_TF32X3));
   const i64 n = Av.rows;
   const i64 rhs = spec.side == RECTRI_CU_LEFT ? Bv.cols : Bv.rows;
 
@@ -1328,6 +1344,7 @@ void gemm_entry(T alpha, int32_t ta_c, const rectri_cu_view& Av, int32_t tb_c,
   validate_view(Bv, "B");
   validate_view(Cv, "C");
   const BackendInfo be = validate_backend(cbe);
+  const Tf32x3Scope tf32x3_scope(std::is_same<T, float>::value && (be.flags & RECTRI_CU_TF32X3));
   if (ta_c < 0 || ta_c > 2 || tb_c < 0 || tb_c > 2) fail(RECTRI_CU_CONFIG, "trans out of range");
   const bool ta = ta_c != RECTRI_CU_NOTRANS, tb = tb_c != RECTRI_CU_NOTRANS;
   const i64 M = Cv.rows, N = Cv.cols;

@@ -269,6 +269,7 @@ void dispatch(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
 
 void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
+  if (tf32x3_enabled() && launch_gemm_f32_tf32x3(p, ta, tb, s)) return;
   dispatch<128, 128, 3>(p, ta, tb, s);
 }
 

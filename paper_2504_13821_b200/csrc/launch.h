@@ -54,6 +54,11 @@ constexpr int kLeafMax = 256;
 
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s);
 void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s);
+// fp32 3xTF32 variant on tcgen05 (sgemm_tf32x3.cu), opt-in: RECTRI_CU_FP32_TF32X3=1.
+bool tf32x3_enabled();
+void tf32x3_set_call(bool on);  // RECTRI_CU_TF32X3 for the calling thread's current call
+bool launch_gemm_f32_tf32x3(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s);
+void tf32x3_reserve(cudaStream_t s, size_t floats);  // per-stream operand-split scratch
 void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s);     // leaf64.cu (v2)
 void launch_leaf_f64_v1(const LeafParams<double>& p, cudaStream_t s);  // leaf.cu
 void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream_t s,

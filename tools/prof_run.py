@@ -26,10 +26,12 @@ if kind in ("trsm", "trmm"):
     rc.fill_uniform(B.view(), seed=2)
     fn = rc.rec_trsm if kind == "trsm" else rc.rec_trmm
     fn(TriangularSpec(), A.cview(), B.view(), Threshold(t), be)
-elif kind in ("gemm", "gemmtn", "sgemm"):
+elif kind in ("gemm", "gemmtn", "sgemm", "tf32x3"):
     M, N, K = args
-    if kind == "sgemm":
+    if kind in ("sgemm", "tf32x3"):
         f64 = torch.float32
+    if kind == "tf32x3":
+        be = Backend.cuda(flags=NO_GRAPH | rc.TF32X3)
     ta = Trans.Trans if kind == "gemmtn" else Trans.NoTrans
     A = MatrixBuffer(K, M, f64, "cuda") if kind == "gemmtn" else MatrixBuffer(M, K, f64, "cuda")
     B = MatrixBuffer(K, N, f64, "cuda")
