@@ -212,18 +212,22 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
         asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[2 * ip][j]), "=f"(acc[2 * ip + 1][j]) : "l"(acc2[ip][j]));
   }
 
+  // Epilogue, per column: every C read of the column issued before the writes.
   const bool beta_zero = p.beta == 0.f;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const i64 n = n0 + FFrag<BN, B_KC>::outer(tx, j);
     if (n >= p.N) continue;
+    float cold[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const i64 m = m0 + FFrag<BM, A_KC>::outer(ty, i);
-      if (m < p.M) {
-        float* c = p.C + m + n * p.ldc;
-        *c = beta_zero ? p.alpha * acc[i][j] : fmaf(p.alpha, acc[i][j], p.beta * *c);
-      }
+      cold[i] = (!beta_zero && m < p.M) ? p.C[m + n * p.ldc] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const i64 m = m0 + FFrag<BM, A_KC>::outer(ty, i);
+      if (m < p.M) p.C[m + n * p.ldc] = beta_zero ? p.alpha * acc[i][j] : fmaf(p.alpha, acc[i][j], p.beta * cold[i]);
     }
   }
 }

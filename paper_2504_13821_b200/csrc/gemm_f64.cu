@@ -50,9 +50,13 @@ int choose(const GemmParams<double>& p) {
 // TMA-fed kernel configuration for a problem, or -1 for the cp.async kernel
 // (identical bits either way).
 // TMA config 1 (64x64 CTAs, producer warp, 4 stages) reaches 36.1-36.4 TF/s
-// (97-98 % of the DMMA peak) from K = 8192 down to K = 1024; below that the
-// cp.async kernels' extra resident warps win (profiles/r01_tma_gemm_sweep.txt).
-int choose_tma(const GemmParams<double>& p) { return p.K >= 1024 ? 1 : -1; }
+// (97-98 % of the DMMA peak) from K = 8192 down to K = 1024 and, with the
+// batched epilogue, also beats the cp.async kernels at K = 512 (29.0 vs 27.5)
+// and K = 256 (19.8 vs 19.3) (profiles/r01_tma_gemm_sweep.txt).
+int choose_tma(const GemmParams<double>& p) {
+  (void)p;
+  return 1;
+}
 
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;

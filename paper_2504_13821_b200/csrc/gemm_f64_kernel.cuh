@@ -276,9 +276,22 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
   }
   cp_async_wait<0>();
 
+  // Epilogue, per row tile: every C read issued before the first write.
   const bool beta_zero = p.beta == 0.0;
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+  for (int i = 0; i < TM; ++i) {
+    double cold[2][TN][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const i64 m = m0 + wm0 + 16 * i + 8 * h + g;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const i64 n = n0 + wn0 + 8 * j + 2 * t;
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          cold[h][j][e] = (!beta_zero && m < p.M && n + e < p.N) ? p.C[m + (n + e) * p.ldc] : 0.0;
+      }
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const i64 m = m0 + wm0 + 16 * i + 8 * h + g;
@@ -289,13 +302,13 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           if (n + e < p.N) {
-            double* c = p.C + m + (n + e) * p.ldc;
             const double v = acc[i][j][2 * h + e];
-            *c = beta_zero ? p.alpha * v : fma(p.alpha, v, p.beta * *c);
+            p.C[m + (n + e) * p.ldc] = beta_zero ? p.alpha * v : fma(p.alpha, v, p.beta * cold[h][j][e]);
           }
         }
       }
     }
+  }
 }
 
 // Host launcher of one configuration (all four transpose forms, both copy

@@ -258,24 +258,36 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
     }
   }
 
-  // Epilogue: C = fma(alpha, acc, beta*C) (beta == 0 never reads C).
+  // Epilogue: C = fma(alpha, acc, beta*C) (beta == 0 never reads C).  Per
+  // output row, every C read is issued before the first write, so the reads'
+  // latency is paid once per row instead of once per element.
   const bool beta_zero = p.beta == 0.0;
+  auto col_of = [&](int j, int e) -> i64 {
+    const int c = 2 * t + e;
+    return n0 + wn0 + (MC_B ? 16 * (j >> 1) + 2 * c + (j & 1) : 8 * j + (((c & 3) << 1) | (c >> 2)));
+  };
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const i64 m = m0 + wm0 + 16 * i + (MC_A ? 2 * g + h : 8 * h + pg);
       if (m >= p.M) continue;
+      double cold[TN][2];
 #pragma unroll
       for (int j = 0; j < TN; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int c = 2 * t + e;
-          const i64 n = n0 + wn0 + (MC_B ? 16 * (j >> 1) + 2 * c + (j & 1) : 8 * j + (((c & 3) << 1) | (c >> 2)));
+          const i64 n = col_of(j, e);
+          cold[j][e] = (!beta_zero && n < p.N) ? p.C[m + n * p.ldc] : 0.0;
+        }
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const i64 n = col_of(j, e);
           if (n < p.N) {
-            double* cp = p.C + m + n * p.ldc;
             const double v = acc[i][j][2 * h + e];
-            *cp = beta_zero ? p.alpha * v : fma(p.alpha, v, p.beta * *cp);
+            p.C[m + n * p.ldc] = beta_zero ? p.alpha * v : fma(p.alpha, v, p.beta * cold[j][e]);
           }
         }
     }

@@ -41,12 +41,22 @@
 namespace rectri_cu {
 namespace tf32x3 {
 
-constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2;
+constexpr int BM = 128, BN = 256;
 constexpr int kThreads = 192;
-constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
-constexpr uint32_t B_TILE = BN * BK * 4;  // 32 KB
-constexpr uint32_t STAGE = 2 * A_TILE + 2 * B_TILE;
-constexpr int kSmem = STAGES * STAGE + 1024 + 256;
+constexpr int kRingBytes = 192 * 1024;  // operand ring: 2 stages of 32-deep or 4 of 16-deep k-tiles
+template <int BK>
+struct Geo {
+  static constexpr uint32_t A_TILE = BM * BK * 4;
+  static constexpr uint32_t B_TILE = BN * BK * 4;
+  static constexpr uint32_t STAGE = 2 * A_TILE + 2 * B_TILE;
+  static constexpr int STAGES = kRingBytes / STAGE;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  // K-major tiles: rows of BK fp32 = BK*4 bytes, 128B (BK 32) / 64B (BK 16) swizzle
+  static constexpr uint32_t K_SBO = 8 * BK * 4;
+  static constexpr uint32_t K_LAYOUT = BK == 32 ? 2u : 4u;
+  // MN-major tiles: 32-element chunks of BK k-rows of 128 bytes
+  static constexpr uint32_t MN_CHUNK = BK * 128;
+};
 
 // ------------------------------------------------------------------ split
 // dst_hi/dst_lo (rows x cols, ld = rows) from a strided view.
@@ -120,11 +130,14 @@ __host__ __device__ constexpr uint32_t instr_desc(bool a_mn, bool b_mn) {
 }
 
 // A_MN: op(A) m-contiguous (A NoTrans); B_MN: op(B) n-contiguous (B Trans).
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int BK>
 __global__ void __launch_bounds__(kThreads, 1)
     tf32x3_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                   const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
                   const GemmParams<float> p, const uint32_t p_lbo_mn, const uint32_t p_sbo_mn) {
+  using G = Geo<BK>;
+  constexpr int STAGES = G::STAGES;
+  constexpr uint32_t STAGE = G::STAGE, A_TILE = G::A_TILE, B_TILE = G::B_TILE;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t bars = sbase + STAGES * STAGE;  // full[s], empty[s], accum
@@ -136,9 +149,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto tile_b = [&](int s, int lo) { return sbase + s * STAGE + 2 * A_TILE + lo * B_TILE; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Grouped rasterization: consecutive CTAs walk 8 M-tiles down one N column,
+  // so the CTAs resident at a time share A row panels and B column panels in L2.
+  constexpr int kGroup = 8;
   const int tiles_m = static_cast<int>(ceil_div(p.M, BM));
-  const int m0 = static_cast<int>(blockIdx.x % tiles_m) * BM;
-  const int n0 = static_cast<int>(blockIdx.x / tiles_m) * BN;
+  const int tiles_n = static_cast<int>(ceil_div(p.N, BN));
+  const int lin = static_cast<int>(blockIdx.x);
+  const int grp = lin / (kGroup * tiles_n), in_grp = lin - grp * kGroup * tiles_n;
+  const int gsize = min(kGroup, tiles_m - grp * kGroup);
+  const int m0 = (grp * kGroup + in_grp % gsize) * BM;
+  const int n0 = (in_grp / gsize) * BN;
   const int KT = static_cast<int>(ceil_div(p.K, BK));
 
   if (threadIdx.x == 0) {
@@ -170,15 +190,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int lo = 0; lo < 2; ++lo) {
           const CUtensorMap* ma = lo ? &mAl : &mAh;
           const CUtensorMap* mb = lo ? &mBl : &mBh;
-          if (A_MN) {  // [m-chunk of 32][k 32][32 m] : box {32, 32}
+          if (A_MN) {  // [m-chunk of 32][k BK][32 m] : box {32, BK}
 #pragma unroll
-            for (int c = 0; c < BM / 32; ++c) tma_2d(tile_a(s, lo) + c * 4096, ma, m0 + 32 * c, k0, full_bar(s));
-          } else {  // [m 128][k 32] rows of 128 B : box {32, 128}
+            for (int c = 0; c < BM / 32; ++c)
+              tma_2d(tile_a(s, lo) + c * G::MN_CHUNK, ma, m0 + 32 * c, k0, full_bar(s));
+          } else {  // [m 128][k BK] : box {BK, 128}
             tma_2d(tile_a(s, lo), ma, k0, m0, full_bar(s));
           }
           if (B_MN) {
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c) tma_2d(tile_b(s, lo) + c * 4096, mb, n0 + 32 * c, k0, full_bar(s));
+            for (int c = 0; c < BN / 32; ++c)
+              tma_2d(tile_b(s, lo) + c * G::MN_CHUNK, mb, n0 + 32 * c, k0, full_bar(s));
           } else {
             tma_2d(tile_b(s, lo), mb, k0, n0, full_bar(s));
           }
@@ -194,13 +216,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n");
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
-          // K-major: +32 bytes per 8-deep k-step inside the 128-byte swizzle row;
+          // K-major: +32 bytes per 8-deep k-step inside the swizzle row;
           // MN-major: +1 KB (8 k-rows of 128 bytes).
           const uint32_t ak = A_MN ? ks * 1024u : ks * 32u;
           const uint32_t bk = B_MN ? ks * 1024u : ks * 32u;
           const uint32_t a_lbo = A_MN ? p_lbo_mn : 16u, b_lbo = B_MN ? p_lbo_mn : 16u;
-          const uint32_t a_sbo = A_MN ? p_sbo_mn : 1024u, b_sbo = B_MN ? p_sbo_mn : 1024u;
-          const uint32_t a_lay = A_MN ? 1u : 2u, b_lay = B_MN ? 1u : 2u;
+          const uint32_t a_sbo = A_MN ? p_sbo_mn : G::K_SBO, b_sbo = B_MN ? p_sbo_mn : G::K_SBO;
+          const uint32_t a_lay = A_MN ? 1u : G::K_LAYOUT, b_lay = B_MN ? 1u : G::K_LAYOUT;
           const uint64_t ah = smem_desc(tile_a(s, 0) + ak, a_lbo, a_sbo, a_lay);
           const uint64_t al = smem_desc(tile_a(s, 1) + ak, a_lbo, a_sbo, a_lay);
           const uint64_t bh = smem_desc(tile_b(s, 0) + bk, b_lbo, b_sbo, b_lay);
@@ -235,17 +257,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
             "=r"(v[30]), "=r"(v[31])
           : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       if (m < p.M) {
+        // all 32 C reads in flight before the first write (one latency per chunk)
+        float cold[32];
+        const i64 nlim = p.N - (n0 + c0);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          cold[j] = (!beta_zero && j < nlim) ? __ldg(p.C + m + (n0 + c0 + j) * p.ldc) : 0.f;
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const i64 n = n0 + c0 + j;
-          if (n < p.N) {
-            float* cp = p.C + m + n * p.ldc;
+          if (j < nlim) {
             const float acc = __uint_as_float(v[j]);
-            *cp = beta_zero ? p.alpha * acc : fmaf(p.alpha, acc, p.beta * *cp);
+            p.C[m + (n0 + c0 + j) * p.ldc] = beta_zero ? p.alpha * acc : fmaf(p.alpha, acc, p.beta * cold[j]);
           }
         }
+      } else {
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       }
     }
   }
@@ -276,15 +304,17 @@ EncodeFn encoder() {
 // Packed column-major X (rows x cols): outer-contiguous operands (MN-major)
 // are (o, k) = X[o + k*rows], box {32, 32}; k-contiguous (K-major) operands
 // are (o, k) = X[k + o*rows], box {32, BO}.
-bool encode(CUtensorMap* map, const float* X, i64 rows, i64 cols, bool mn, int BO) {
+bool encode(CUtensorMap* map, const float* X, i64 rows, i64 cols, bool mn, int BO, int BK) {
   EncodeFn enc = encoder();
   if (!enc) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(rows) * 4};
-  const cuuint32_t box[2] = {32u, mn ? 32u : static_cast<cuuint32_t>(BO)};
+  const cuuint32_t box[2] = {mn ? 32u : static_cast<cuuint32_t>(BK), mn ? static_cast<cuuint32_t>(BK)
+                                                                          : static_cast<cuuint32_t>(BO)};
   const cuuint32_t estr[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : (BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -326,16 +356,29 @@ void split(const float* X, i64 ld, i64 rows, i64 cols, float* hi, float* lo, cud
   ++launch_counter();
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int BK>
 void launch(const CUtensorMap* maps, const GemmParams<float>& p, cudaStream_t s) {
-  auto kern = tf32x3_kernel<A_MN, B_MN>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  auto kern = tf32x3_kernel<A_MN, B_MN, BK>;
+  constexpr int smem = Geo<BK>::SMEM;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const unsigned grid = static_cast<unsigned>(ceil_div(p.M, BM) * ceil_div(p.N, BN));
-  // MN-major descriptor offsets (RECTRI_CU_TF32X3_MN="lbo,sbo" overrides, for bring-up)
-  uint32_t lbo = 4096, sbo = 512;
-  if (const char* e = getenv("RECTRI_CU_TF32X3_MN")) sscanf(e, "%u,%u", &lbo, &sbo);
-  kern<<<grid, kThreads, kSmem, s>>>(maps[0], maps[1], maps[2], maps[3], p, lbo, sbo);
+  // MN-major descriptor offsets: LBO = 32-element chunk stride, SBO = 4-row k-group stride
+  const uint32_t lbo = Geo<BK>::MN_CHUNK, sbo = 512;
+  kern<<<grid, kThreads, smem, s>>>(maps[0], maps[1], maps[2], maps[3], p, lbo, sbo);
   ++launch_counter();
+}
+
+int k_depth() {
+  const char* e = getenv("RECTRI_CU_TF32X3_BK");  // 16 (default, 4 stages) or 32 (2 stages)
+  return e && atoi(e) == 32 ? 32 : 16;
+}
+
+template <int BK>
+void launch_bk(bool a_mn, bool b_mn, const CUtensorMap* maps, const GemmParams<float>& p, cudaStream_t s) {
+  if (a_mn && b_mn) launch<true, true, BK>(maps, p, s);
+  else if (a_mn) launch<true, false, BK>(maps, p, s);
+  else if (b_mn) launch<false, true, BK>(maps, p, s);
+  else launch<false, false, BK>(maps, p, s);
 }
 
 }  // namespace tf32x3
@@ -373,13 +416,12 @@ bool launch_gemm_f32_tf32x3(const GemmParams<float>& p, bool ta, bool tb, cudaSt
   const i64 arp = ar, brp = br;
   const bool a_mn = !ta, b_mn = tb;
   CUtensorMap maps[4];
-  if (!encode(&maps[0], ah, arp, ac, a_mn, BM) || !encode(&maps[1], al, arp, ac, a_mn, BM) ||
-      !encode(&maps[2], bh, brp, bc, b_mn, BN) || !encode(&maps[3], bl, brp, bc, b_mn, BN))
+  const int bk = k_depth();
+  if (!encode(&maps[0], ah, arp, ac, a_mn, BM, bk) || !encode(&maps[1], al, arp, ac, a_mn, BM, bk) ||
+      !encode(&maps[2], bh, brp, bc, b_mn, BN, bk) || !encode(&maps[3], bl, brp, bc, b_mn, BN, bk))
     return false;
-  if (a_mn && b_mn) launch<true, true>(maps, p, s);
-  else if (a_mn) launch<true, false>(maps, p, s);
-  else if (b_mn) launch<false, true>(maps, p, s);
-  else launch<false, false>(maps, p, s);
+  if (bk == 32) launch_bk<32>(a_mn, b_mn, maps, p, s);
+  else launch_bk<16>(a_mn, b_mn, maps, p, s);
   return true;
 }
 
