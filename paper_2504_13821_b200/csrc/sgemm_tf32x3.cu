@@ -83,7 +83,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
   long long spins = 0;
   while (!ok) {
-    if (++spins > (1ll << 30)) __trap();  // a lost arrival aborts the kernel instead of hanging the GPU
+    if (++spins > (1ll << 26)) __trap();  // a lost arrival aborts the kernel instead of hanging the GPU
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
@@ -257,14 +257,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
             "=r"(v[30]), "=r"(v[31])
           : "r"(taddr));
-      if (m < p.M) {
-        // all 32 C reads in flight before the first write (one latency per chunk)
-        float cold[32];
-        const i64 nlim = p.N - (n0 + c0);
+      // all 32 C reads in flight before the first write (one latency per chunk)
+      float cold[32];
+      const i64 nlim = p.N - (n0 + c0);
+      const bool row_ok = m < p.M;
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          cold[j] = (!beta_zero && j < nlim) ? __ldg(p.C + m + (n0 + c0 + j) * p.ldc) : 0.f;
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      for (int j = 0; j < 32; ++j)
+        cold[j] = (row_ok && !beta_zero && j < nlim) ? __ldg(p.C + m + (n0 + c0 + j) * p.ldc) : 0.f;
+      __syncwarp();
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");  // warp-converged (.aligned)
+      if (row_ok) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           if (j < nlim) {
@@ -272,8 +274,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             p.C[m + (n0 + c0 + j) * p.ldc] = beta_zero ? p.alpha * acc : fmaf(p.alpha, acc, p.beta * cold[j]);
           }
         }
-      } else {
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       }
     }
   }
