@@ -242,19 +242,21 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
       const int cb = kk & 1, nb = cb ^ 1;
       if (kk < 3) {
         load_frags(nb, s, kk + 1);
-      } else {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty_bar(s));  // this warp is done reading stage s
-        if (kt + 1 < KT) {
-          const int s1 = (kt + 1) % STAGES;
-          mbar_wait(full_bar(s1), ((kt + 1) / STAGES) & 1);
-          load_frags(nb, s1, 0);
-        }
+      } else if (kt + 1 < KT) {
+        const int s1 = (kt + 1) % STAGES;
+        mbar_wait(full_bar(s1), ((kt + 1) / STAGES) & 1);
+        load_frags(nb, s1, 0);
       }
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) dmma1684(acc[i][j], af[cb][i][0], af[cb][i][1], bf[cb][j]);
+      if (kk == 3) {
+        // The last MMAs of the tile have consumed every fragment read from
+        // stage s (so those shared loads are complete): release the stage.
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_bar(s));
+      }
     }
   }
 

@@ -74,7 +74,9 @@ void launch_leaf3_pack(const LeafParams<double>& p, double* dst, cudaStream_t s)
 int leaf_version();  // RECTRI_CU_LEAF (fp64: 1 = leaf.cu, 2 = leaf64.cu, 3 = leaf64_v3.cu)
 // Allocates the v2 fp64 leaf's per-stream scratch (call before capturing on s).
 void leaf_scratch_reserve(cudaStream_t s);
-void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s);
+void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s);     // leaf64.cu dispatch
+void launch_leaf_f32_v1(const LeafParams<float>& p, cudaStream_t s);  // leaf.cu
+void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t s);  // leaf32_v3.cu
 
 // B[rows x cols] (ld) <- alpha * B.
 void launch_scale_f64(double* B, i64 ld, i64 rows, i64 cols, double alpha, cudaStream_t s);

@@ -477,6 +477,6 @@ void launch_leaf(const LeafParams<T>& p_in, cudaStream_t s) {
 }  // namespace
 
 void launch_leaf_f64_v1(const LeafParams<double>& p, cudaStream_t s) { launch_leaf<double>(p, s); }
-void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s) { launch_leaf<float>(p, s); }
+void launch_leaf_f32_v1(const LeafParams<float>& p, cudaStream_t s) { launch_leaf<float>(p, s); }
 
 }  // namespace rectri_cu

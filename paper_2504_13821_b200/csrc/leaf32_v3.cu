@@ -1,0 +1,290 @@
+// leaf32_v3.cu -- fp32 base (leaf) kernel v3: the fp64 v3 design
+// (leaf64_v3.cu) on the FFMA pipe.
+//
+// trsm_base / trmm_base (src/base_kernels.cpp:94-177) on the Left form of a
+// virtual lower factor L' in 32-row blocks:
+//   * pack32_kernel writes, per leaf call, the blocks in consumption order as
+//     [k][row] fp32 tiles (TRSM row I: L'_I0 .. L'_I,I-1, then -inv(L'_II);
+//     TRMM rows descending: ..., then L'_II with its diagonal).  The inverse
+//     is computed in fp64 by substitution (one thread per column) and rounded
+//     once; masked / out-of-range entries are exact zeros by selection and
+//     padding rows get an identity diagonal.
+//   * leaf32_kernel: one CTA owns 32 right-hand sides (panel nb x 32 floats
+//     in shared memory); a producer warp streams the packed blocks through an
+//     8-deep cp.async.bulk ring (mbarrier full/empty); 8 compute warps each
+//     own 4 rows x 1 right-hand side (lane) of the current 32x32 row block and
+//     accumulate with packed FFMA2 (fma.rn.f32x2: two rows per instruction,
+//     the L' pair read as one broadcast ld.shared.v4 per k).
+// Results agree with leaf.cu (v1, RECTRI_CU_LEAF=1) to rounding.
+#include <cstdlib>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace rectri_cu {
+namespace leaf32v3 {
+
+constexpr int kRB = 32;
+constexpr int kNC = 32;
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kBlk = kRB * kRB;  // floats per packed block
+constexpr int kRing = 8;
+constexpr int kSmem = (kLeafMax * kNC + kRB * kNC + kRing * kBlk) * 4 + 2 * kRing * 8;
+
+__device__ __forceinline__ float lprime(const LeafParams<float>& p, int r, int j) {
+  const int rr = p.reflected ? p.n - 1 - r : r;
+  const int jj = p.reflected ? p.n - 1 - j : j;
+  const i64 row = p.swapped ? jj : rr;
+  const i64 col = p.swapped ? rr : jj;
+  return p.A[row + col * p.lda];
+}
+
+__device__ __forceinline__ int seq_of(int I, int J, int nblk, bool asc) {
+  if (asc) return I * (I + 1) / 2 + J;
+  return (nblk * (nblk + 1) / 2 - (I + 1) * (I + 2) / 2) + J;
+}
+
+__global__ void __launch_bounds__(256) pack32_kernel(const LeafParams<float> p, float* __restrict__ P) {
+  __shared__ double L[kRB][kRB + 1];
+  const int nblk = (p.n + kRB - 1) / kRB;
+  const bool trsm = p.trsm != 0;
+  const int b = blockIdx.x;
+  int I = 0;
+  while ((I + 1) * (I + 2) / 2 <= b) ++I;
+  const int J = b - I * (I + 1) / 2;
+  const int r0 = I * kRB, j0 = J * kRB;
+  float* dst = P + static_cast<size_t>(seq_of(I, J, nblk, trsm)) * kBlk;
+  const int tid = threadIdx.x;
+  if (J < I) {  // [k][r]
+    for (int o = tid; o < kBlk; o += blockDim.x) {
+      const int k = o >> 5, r = o & 31;
+      dst[o] = r0 + r < p.n ? lprime(p, r0 + r, j0 + k) : 0.f;
+    }
+    return;
+  }
+  for (int o = tid; o < kBlk; o += blockDim.x) {
+    const int r = o >> 5, k = o & 31;
+    double v = 0.0;
+    if (r0 + r >= p.n) v = r == k ? 1.0 : 0.0;
+    else if (k < r) v = lprime(p, r0 + r, r0 + k);
+    else if (k == r) v = p.unit ? 1.0 : lprime(p, r0 + r, r0 + r);
+    L[r][k] = v;
+  }
+  __syncthreads();
+  if (!trsm) {
+    for (int o = tid; o < kBlk; o += blockDim.x) {
+      const int k = o >> 5, r = o & 31;
+      dst[o] = static_cast<float>(L[r][k]);
+    }
+    return;
+  }
+  if (tid < kRB) {  // -inv(L), column j = tid, in fp64
+    const int j = tid;
+    double y[kRB];
+#pragma unroll
+    for (int r = 0; r < kRB; ++r) {
+      double s = r == j ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < r; ++q) s = fma(-L[r][q], y[q], s);
+      y[r] = r < j ? 0.0 : s / L[r][r];
+    }
+#pragma unroll
+    for (int r = 0; r < kRB; ++r) dst[j * kRB + r] = static_cast<float>(-y[r]);  // [k = j][r]
+  }
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads + 32, 3) leaf32_kernel(const LeafParams<float> p,
+                                                                 const float* __restrict__ P) {
+  extern __shared__ __align__(128) float smem32[];
+  float* panel = smem32;                  // [r][32]
+  float* cbuf = panel + kLeafMax * kNC;   // [r][32]
+  float* ring = cbuf + kRB * kNC;         // kRing blocks [k][r]
+  const uint32_t full0 = smem_u32(ring + kRing * kBlk), empty0 = full0 + 8 * kRing;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = p.n;
+  const int nblk = (n + kRB - 1) / kRB;
+  const int rows_p = nblk * kRB;
+  const i64 c0 = static_cast<i64>(blockIdx.x) * kNC;
+  const int ncols = static_cast<int>(min(static_cast<i64>(kNC), p.nrhs - c0));
+  const bool trsm = p.trsm != 0;
+
+  // Panel visitor (compute warps): Left -> each warp covers 4 rows x 8
+  // right-hand sides; Right -> one row of 32 per warp.
+  const i64 rstep = p.reflected ? -1 : 1;
+  auto for_panel = [&](auto&& f) {
+    if (!p.right) {
+      const int rl = lane & 3, cl = lane >> 2;
+#pragma unroll
+      for (int cg = 0; cg < kNC / 8; ++cg) {
+        const int c = 8 * cg + cl;
+        const float* colp = p.B + (c0 + c) * p.ldb + (p.reflected ? n - 1 : 0);
+        for (int rt = warp; rt < rows_p / 4; rt += kWarps) {
+          const int r = 4 * rt + rl;
+          f(r, c, colp + r * rstep);
+        }
+      }
+    } else {
+      const int c = lane;
+      for (int r = warp; r < rows_p; r += kWarps) {
+        const i64 sr = p.reflected ? n - 1 - r : r;
+        f(r, c, p.B + sr * p.ldb + c0 + c);
+      }
+    }
+  };
+
+  if (!trsm && p.alpha == 0.f) {  // base_kernels.cpp:143-150
+    if (warp < kWarps)
+      for_panel([&](int r, int c, const float* g) {
+        if (r < n && c < ncols) *const_cast<float*>(g) = 0.f;
+      });
+    return;
+  }
+  const int nseq = nblk * (nblk + 1) / 2;
+  if (tid == 0) {
+    for (int q = 0; q < kRing; ++q) {
+      mbar_init(full0 + 8 * q, 1);
+      mbar_init(empty0 + 8 * q, kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kWarps) {  // producer warp
+    if (lane == 0)
+      for (int q = 0; q < nseq; ++q) {
+        const int slot = q % kRing;
+        if (q >= kRing) mbar_wait(empty0 + 8 * slot, ((q / kRing) + 1) & 1);
+        mbar_expect_tx(full0 + 8 * slot, kBlk * 4);
+        bulk_g2s(smem_u32(ring + slot * kBlk), P + static_cast<size_t>(q) * kBlk, kBlk * 4, full0 + 8 * slot);
+      }
+    return;
+  }
+  for_panel([&](int r, int c, const float* g) {
+    const bool ok = r < n && c < ncols;
+    cp_async4(panel + r * kNC + c, ok ? g : p.B, ok ? 4 : 0);
+  });
+  cp_async_commit();
+  cp_async_wait<0>();
+  named_sync(1, kThreads);
+  if (trsm && p.alpha != 1.f) {  // x = alpha * b (base_kernels.cpp:76-77)
+    for_panel([&](int r, int c, const float*) { panel[r * kNC + c] *= p.alpha; });
+    named_sync(1, kThreads);
+  }
+
+  // Thread (warp w, lane c): rows 4w .. 4w+3 of the row block, right-hand side c.
+  const int rw = 4 * warp, cc = lane;
+  unsigned long long acc[2];  // packed pairs (rows 4w, 4w+1), (4w+2, 4w+3)
+  int s = 0;
+  auto block_mma = [&](const float* src) {  // acc += block(s) * src[32 x 32 rows][cc]
+    const int slot = s % kRing;
+    mbar_wait(full0 + 8 * slot, (s / kRing) & 1);
+    const float* blk = ring + slot * kBlk;
+#pragma unroll 8
+    for (int k = 0; k < kRB; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(blk + k * kRB + rw);  // broadcast
+      const float x = src[k * kNC + cc];
+      unsigned long long a01, a23;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(a01) : "f"(a.x), "f"(a.y));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(a23) : "f"(a.z), "f"(a.w));
+      unsigned long long xx;
+      asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
+      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[0]) : "l"(a01), "l"(xx));
+      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[1]) : "l"(a23), "l"(xx));
+    }
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive(empty0 + 8 * slot);
+    }
+    ++s;
+  };
+  auto unpack = [&](float (&v)[4]) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(acc[0]));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(acc[1]));
+  };
+  auto pack = [&](const float (&v)[4]) {
+    asm("mov.b64 %0, {%1, %2};" : "=l"(acc[0]) : "f"(v[0]), "f"(v[1]));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(acc[1]) : "f"(v[2]), "f"(v[3]));
+  };
+
+  for (int bi = 0; bi < nblk; ++bi) {
+    const int I = trsm ? bi : nblk - 1 - bi;
+    const int r0 = I * kRB;
+    float v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = trsm ? -panel[(r0 + rw + i) * kNC + cc] : 0.f;
+    pack(v);
+    for (int J = 0; J < I; ++J) block_mma(panel + J * kRB * kNC);
+    if (trsm) {
+      // acc = -(b_I - sum L'X); X_I = (-inv(L'_II)) * acc
+      unpack(v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cbuf[(rw + i) * kNC + cc] = v[i];
+      named_sync(1, kThreads);
+      acc[0] = acc[1] = 0ull;
+      block_mma(cbuf);
+      unpack(v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) panel[(r0 + rw + i) * kNC + cc] = v[i];
+      named_sync(1, kThreads);  // X_I visible; cbuf free
+    } else {
+      block_mma(panel + I * kRB * kNC);  // + L'_II * b_I
+      named_sync(1, kThreads);           // every warp has read b_I
+      unpack(v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) panel[(r0 + rw + i) * kNC + cc] = p.alpha * v[i];
+    }
+  }
+  named_sync(1, kThreads);
+  for_panel([&](int r, int c, const float* g) {
+    if (r < n && c < ncols) *const_cast<float*>(g) = panel[r * kNC + c];
+  });
+}
+
+}  // namespace leaf32v3
+
+void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t s) {
+  using namespace leaf32v3;
+  const int nblk = (p.n + kRB - 1) / kRB;
+  if (p.trsm || p.alpha != 0.f) {
+    pack32_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, scratch);
+    ++launch_counter();
+  }
+  const unsigned grid = static_cast<unsigned>(ceil_div(p.nrhs, kNC));
+  cudaFuncSetAttribute(leaf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  leaf32_kernel<<<grid, kThreads + 32, kSmem, s>>>(p, scratch);
+  ++launch_counter();
+}
+
+}  // namespace rectri_cu

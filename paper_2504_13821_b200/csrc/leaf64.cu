@@ -461,6 +461,18 @@ int leaf_version_env() {
 
 int leaf_version() { return leaf64::leaf_version_env(); }
 
+void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s) {
+  if (p.n <= 0 || p.nrhs <= 0) return;
+  double* P = nullptr;
+  if (leaf64::leaf_version_env() >= 3) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    P = leaf64::scratch_for(s, cs == cudaStreamCaptureStatusNone);  // >= the fp32 blocks' bytes
+  }
+  if (P) launch_leaf_f32_v3(p, reinterpret_cast<float*>(P), s);
+  else launch_leaf_f32_v1(p, s);
+}
+
 void leaf_scratch_reserve(cudaStream_t s) { leaf64::scratch_for(s, true); }
 
 void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s) {

@@ -279,16 +279,18 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
 #pragma unroll
       for (int e = 0; e < 2; ++e)
         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(bv[kk][e]) : "r"(bsrc + b_base[e] + kk * 4 * kNC * 8));
-    __syncwarp();
-    if (lane == 0) {  // fragments are in registers: release the slot to the async (bulk-copy) proxy
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      mbar_arrive(empty0 + 8 * slot);
-    }
-    ++s;
 #pragma unroll
     for (int kk = 0; kk < kRB / 4; ++kk)
 #pragma unroll
       for (int e = 0; e < 2; ++e) dmma884(c[e][0], c[e][1], a[kk], bv[kk][e]);
+    // The DMMAs have consumed every fragment loaded from the slot, so those
+    // loads are complete: only now release the slot to the bulk-copy proxy.
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive(empty0 + 8 * slot);
+    }
+    ++s;
   };
 
   for (int bi = 0; bi < nblk; ++bi) {

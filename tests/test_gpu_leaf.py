@@ -87,3 +87,21 @@ def test_leaf_masking_and_alpha_zero(cuda, monkeypatch, version):
     b = F(np.full((n, m), np.nan))
     got = _base("trmm", s, F(rng.uniform(-1, 1, (n, n))), b, version, monkeypatch)
     assert np.all(got == 0.0)
+
+
+@pytest.mark.parametrize("op", ["trsm", "trmm"])
+@pytest.mark.parametrize("side,uplo,trans,diag", VARIANTS)
+def test_leaf32_v3_matches_v1_and_oracle(cuda, monkeypatch, op, side, uplo, trans, diag):
+    """fp32 leaf v3 (leaf32_v3.cu: packed blocks, FFMA2, inverse diagonal
+    blocks in fp64 rounded once) against the oracle and v1 (leaf.cu)."""
+    rng = np.random.default_rng(300 + 8 * side + 4 * uplo + 2 * trans + diag)
+    eps = np.finfo(np.float32).eps
+    for n, m, alpha in ((1, 3, 1.0), (33, 70, 1.0), (100, 65, -0.75), (256, 96, 1.0)):
+        s = oracle.spec(side, uplo, trans, diag, alpha)
+        a, b = _inputs(op, s, n, m, rng)
+        a, b = F(a.astype(np.float32)), F(b.astype(np.float32))
+        v1 = _base(op, s, a, b, 1, monkeypatch)
+        v3 = _base(op, s, a, b, 3, monkeypatch)
+        check_against_oracle(op, s, a, b, v3)
+        scale = max(1.0, float(np.max(np.abs(v1))))
+        assert float(np.max(np.abs(v3 - v1))) <= 64 * n * eps * scale, (n, m)
