@@ -244,7 +244,7 @@ struct Backend {
   GemmBlocking blocking{};
   int device = -1;          // CUDA ordinal, -1 = current
   void* stream = nullptr;   // cudaStream_t, nullptr = legacy default stream
-  std::uint32_t flags = 0;  // RECTRI_CU_ASYNC | RECTRI_CU_NO_GRAPH
+  std::uint32_t flags = 0;  // RECTRI_CU_ASYNC | RECTRI_CU_NO_GRAPH | RECTRI_CU_TF32X3
 
   static Backend seq() { return Backend{}; }
   static Backend par(int width = 0) {
