@@ -407,13 +407,32 @@ def main():
     roofline = {
         "bound": "tensor", "achieved": gemm_tflops, "peak": peak64, "unit": "TFLOP/s",
         "frac": gemm_tflops / peak64 if peak64 > 0 else None, "traffic": traffic,
-        "kernel": "dgemm_dmma_kernel (off-diagonal GEMM updates, DMMA.8x8x4)",
+        "kernel": "dgemm_tma_kernel (off-diagonal GEMM updates, TMA-fed DMMA.8x8x4)",
         "peak_source": "live DMMA.8x8x4 issue-rate probe on this GPU (rectri_cu_probe_peak; MEASURED_PEAKS.json "
                        "has no fp64 figure); cf. profiles/r01_microbench_peaks.jsonl",
         "per_launch_flops": g["flops"] / max(g["launches"], 1), "launches": g["launches"],
         "share_of_step": g["ms"] / step_ms_prof if step_ms_prof else None,
         "breakdown_ms": {k: v["ms"] for k, v in prof.items()},
     }
+    # The leaf (trsm_base per diagonal block): achieved HBM bandwidth on its
+    # algorithmic bytes (nb(nb+1)/2 + 2 nb r) * 8 next to the
+    # measured copy bandwidth -- it is latency / tensor bound, not HBM bound.
+    lf = prof.get("leaf", {})
+    if lf.get("launches"):
+        nleaf = lf["launches"]
+        nb = n // nleaf if n % nleaf == 0 else args.threshold
+        leaf_bytes = (nb * (nb + 1) // 2 + 2 * nb * m) * 8 * nleaf
+        hbm = 6450.0
+        try:
+            hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", hbm))
+        except Exception:
+            pass
+        roofline["leaf"] = {
+            "kernel": "leaf3_kernel (fp64 trsm_base, packed-block ring, DMMA)", "launches": nleaf,
+            "ms": lf["ms"], "algorithmic_bytes": leaf_bytes,
+            "achieved_gbs": leaf_bytes / (lf["ms"] * 1e-3) / 1e9 if lf["ms"] else None,
+            "hbm_peak_gbs": hbm, "achieved_tflops": lf["flops"] / (lf["ms"] * 1e-3) / 1e12 if lf["ms"] else None,
+        }
 
     # End to end through the C-ABI with pinned host buffers.
     e2e = None
