@@ -419,7 +419,7 @@ void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaSt
   p.unit = spec.diag == RECTRI_CU_UNIT ? 1 : 0;
   p.trsm = op == kTrsm ? 1 : 0;
   p.alpha = static_cast<T>(spec.alpha);
-  if constexpr (std::is_same<T, double>::value) p.packed = packed;
+  p.packed = packed;
   ProfScope prof(1, static_cast<double>(n) * n * rhs, s);
   K<T>::leaf(p, s);
 }
@@ -560,9 +560,9 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
   if (op == kTrsm) eff.alpha = 1.0;
   // fp64 v3 leaves: pack every leaf's triangle once, up front, for all
   // right-hand-side streams (allocations before any capture).
-  LeafParams<double> pbase{};
+  LeafParams<T> pbase{};
   int nleaves = 0;
-  if constexpr (std::is_same<T, double>::value) {
+  {
     if (leaf_version() >= 3 && threshold <= kLeafMax && !(op == kTrmm && spec.alpha == 0.0)) {
       std::vector<std::pair<i64, i64>> lv;
       Recursion<T>(op, threshold, nullptr, nullptr, &lv, true).run(eff, A, B, 0);
@@ -590,7 +590,7 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
       pbase.swapped = effop == 1 ? 1 : 0;
       pbase.unit = spec.diag == RECTRI_CU_UNIT ? 1 : 0;
       pbase.trsm = op == kTrsm ? 1 : 0;
-      pbase.alpha = eff.alpha;
+      pbase.alpha = static_cast<T>(eff.alpha);
     }
   }
   i64& counter = launch_counter();
@@ -615,7 +615,13 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
   }
   if (nleaves > 0) {
     long long* d_r0 = static_cast<long long*>(g->leaf_meta);
-    launch_leaf3_pack_all(pbase, d_r0, reinterpret_cast<int*>(d_r0 + nleaves), nleaves, g->packed, s);
+    int* d_n = reinterpret_cast<int*>(d_r0 + nleaves);
+    if constexpr (std::is_same<T, double>::value)
+      launch_leaf3_pack_all(pbase, d_r0, d_n, nleaves, g->packed, s);
+    else
+      // slices at the same byte stride as the recursion's double* arithmetic
+      launch_leaf32_pack_all(pbase, d_r0, d_n, nleaves, reinterpret_cast<float*>(g->packed),
+                             2 * static_cast<long long>(leaf3_scratch_doubles()), s);
   }
   auto with_packs = [&](Recursion<T>& r) -> Recursion<T>& {
     if (nleaves > 0) {

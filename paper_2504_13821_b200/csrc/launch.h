@@ -76,7 +76,10 @@ int leaf_version();  // RECTRI_CU_LEAF (fp64: 1 = leaf.cu, 2 = leaf64.cu, 3 = le
 void leaf_scratch_reserve(cudaStream_t s);
 void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s);     // leaf64.cu dispatch
 void launch_leaf_f32_v1(const LeafParams<float>& p, cudaStream_t s);  // leaf.cu
-void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t s);  // leaf32_v3.cu
+void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t s,
+                        bool prepacked = false);  // leaf32_v3.cu
+void launch_leaf32_pack_all(const LeafParams<float>& base, const long long* d_r0, const int* d_n, int nleaves,
+                            float* scratch, long long stride, cudaStream_t s);
 
 // B[rows x cols] (ld) <- alpha * B.
 void launch_scale_f64(double* B, i64 ld, i64 rows, i64 cols, double alpha, cudaStream_t s);

@@ -13,8 +13,10 @@
 //     in shared memory); a producer warp streams the packed blocks through an
 //     8-deep cp.async.bulk ring (mbarrier full/empty); 8 compute warps each
 //     own 4 rows x 1 right-hand side (lane) of the current 32x32 row block and
-//     accumulate with packed FFMA2 (fma.rn.f32x2: two rows per instruction,
-//     the L' pair read as one broadcast ld.shared.v4 per k).
+//     accumulate with packed FFMA2 (fma.rn.f32x2: two rows per instruction);
+//     per 4 k-steps a lane reads its 4 right-hand-side values as one
+//     ld.shared.v4 (column-major padded panel) and the 4 x 4 L' values as
+//     four broadcast ld.shared.v4.
 // Results agree with leaf.cu (v1, RECTRI_CU_LEAF=1) to rounding.
 #include <cstdlib>
 
@@ -30,7 +32,12 @@ constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kBlk = kRB * kRB;  // floats per packed block
 constexpr int kRing = 8;
-constexpr int kSmem = (kLeafMax * kNC + kRB * kNC + kRing * kBlk) * 4 + 2 * kRing * 8;
+// Panel and partial-result buffers are column-major per right-hand side
+// ([c][r]) with padded strides, so a lane reads 4 consecutive rows of its
+// column as one conflict-free ld.shared.v4 (bank = 4c + r mod 32).
+constexpr int kPS = kLeafMax + 4;  // panel column stride (floats)
+constexpr int kCS = kRB + 4;       // cbuf column stride
+constexpr int kSmem = (kNC * kPS + kNC * kCS + kRing * kBlk) * 4 + 2 * kRing * 8;
 
 __device__ __forceinline__ float lprime(const LeafParams<float>& p, int r, int j) {
   const int rr = p.reflected ? p.n - 1 - r : r;
@@ -45,11 +52,10 @@ __device__ __forceinline__ int seq_of(int I, int J, int nblk, bool asc) {
   return (nblk * (nblk + 1) / 2 - (I + 1) * (I + 2) / 2) + J;
 }
 
-__global__ void __launch_bounds__(256) pack32_kernel(const LeafParams<float> p, float* __restrict__ P) {
+__device__ void pack32_block(const LeafParams<float>& p, float* __restrict__ P, const int b) {
   __shared__ double L[kRB][kRB + 1];
   const int nblk = (p.n + kRB - 1) / kRB;
   const bool trsm = p.trsm != 0;
-  const int b = blockIdx.x;
   int I = 0;
   while ((I + 1) * (I + 2) / 2 <= b) ++I;
   const int J = b - I * (I + 1) / 2;
@@ -94,6 +100,24 @@ __global__ void __launch_bounds__(256) pack32_kernel(const LeafParams<float> p, 
   }
 }
 
+__global__ void __launch_bounds__(256) pack32_kernel(const LeafParams<float> p, float* __restrict__ P) {
+  pack32_block(p, P, blockIdx.x);
+}
+
+// Every leaf of one recursion (blockIdx.y = leaf k: order ns[k] at
+// A(r0s[k], r0s[k])) into P + k * stride.
+__global__ void __launch_bounds__(256) pack32_all_kernel(const LeafParams<float> base, const long long* __restrict__ r0s,
+                                                         const int* __restrict__ ns, float* __restrict__ P,
+                                                         long long stride) {
+  const int k = blockIdx.y;
+  LeafParams<float> p = base;
+  p.n = ns[k];
+  p.A = base.A + r0s[k] * (1 + base.lda);
+  const int nblk = (p.n + kRB - 1) / kRB;
+  if (static_cast<int>(blockIdx.x) >= nblk * (nblk + 1) / 2) return;
+  pack32_block(p, P + static_cast<size_t>(k) * stride, blockIdx.x);
+}
+
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
 }
@@ -127,9 +151,9 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 __global__ void __launch_bounds__(kThreads + 32, 3) leaf32_kernel(const LeafParams<float> p,
                                                                  const float* __restrict__ P) {
   extern __shared__ __align__(128) float smem32[];
-  float* panel = smem32;                  // [r][32]
-  float* cbuf = panel + kLeafMax * kNC;   // [r][32]
-  float* ring = cbuf + kRB * kNC;         // kRing blocks [k][r]
+  float* panel = smem32;                  // [c][r], stride kPS
+  float* cbuf = panel + kNC * kPS;        // [c][r], stride kCS
+  float* ring = cbuf + kNC * kCS;         // kRing blocks [k][r]
   const uint32_t full0 = smem_u32(ring + kRing * kBlk), empty0 = full0 + 8 * kRing;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = p.n;
@@ -192,13 +216,13 @@ __global__ void __launch_bounds__(kThreads + 32, 3) leaf32_kernel(const LeafPara
   }
   for_panel([&](int r, int c, const float* g) {
     const bool ok = r < n && c < ncols;
-    cp_async4(panel + r * kNC + c, ok ? g : p.B, ok ? 4 : 0);
+    cp_async4(panel + c * kPS + r, ok ? g : p.B, ok ? 4 : 0);
   });
   cp_async_commit();
   cp_async_wait<0>();
   named_sync(1, kThreads);
   if (trsm && p.alpha != 1.f) {  // x = alpha * b (base_kernels.cpp:76-77)
-    for_panel([&](int r, int c, const float*) { panel[r * kNC + c] *= p.alpha; });
+    for_panel([&](int r, int c, const float*) { panel[c * kPS + r] *= p.alpha; });
     named_sync(1, kThreads);
   }
 
@@ -206,22 +230,28 @@ __global__ void __launch_bounds__(kThreads + 32, 3) leaf32_kernel(const LeafPara
   const int rw = 4 * warp, cc = lane;
   unsigned long long acc[2];  // packed pairs (rows 4w, 4w+1), (4w+2, 4w+3)
   int s = 0;
-  auto block_mma = [&](const float* src) {  // acc += block(s) * src[32 x 32 rows][cc]
+  // acc += block(s) * src(32 rows of column cc, consecutive floats)
+  auto block_mma = [&](const float* src) {
     const int slot = s % kRing;
     mbar_wait(full0 + 8 * slot, (s / kRing) & 1);
     const float* blk = ring + slot * kBlk;
-#pragma unroll 8
-    for (int k = 0; k < kRB; ++k) {
-      const float4 a = *reinterpret_cast<const float4*>(blk + k * kRB + rw);  // broadcast
-      const float x = src[k * kNC + cc];
-      unsigned long long a01, a23;
-      asm("mov.b64 %0, {%1, %2};" : "=l"(a01) : "f"(a.x), "f"(a.y));
-      asm("mov.b64 %0, {%1, %2};" : "=l"(a23) : "f"(a.z), "f"(a.w));
-      unsigned long long xx;
-      asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
-      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[0]) : "l"(a01), "l"(xx));
-      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[1]) : "l"(a23), "l"(xx));
+#pragma unroll
+    for (int kb = 0; kb < kRB; kb += 4) {
+      const float4 x4 = *reinterpret_cast<const float4*>(src + kb);
+      const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const float4 a = *reinterpret_cast<const float4*>(blk + (kb + kk) * kRB + rw);  // broadcast
+        unsigned long long a01, a23, xx;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(a01) : "f"(a.x), "f"(a.y));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(a23) : "f"(a.z), "f"(a.w));
+        asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(xs[kk]));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[0]) : "l"(a01), "l"(xx));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[1]) : "l"(a23), "l"(xx));
+      }
     }
+    // every fragment read from the slot has been consumed by an FFMA2 above;
+    // order those generic-proxy reads before the async-proxy refill
     __syncwarp();
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -238,46 +268,60 @@ __global__ void __launch_bounds__(kThreads + 32, 3) leaf32_kernel(const LeafPara
     asm("mov.b64 %0, {%1, %2};" : "=l"(acc[1]) : "f"(v[2]), "f"(v[3]));
   };
 
+  float* pcol = panel + cc * kPS;  // this lane's right-hand side, rows contiguous
+  float* ccol = cbuf + cc * kCS;
   for (int bi = 0; bi < nblk; ++bi) {
     const int I = trsm ? bi : nblk - 1 - bi;
     const int r0 = I * kRB;
     float v[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = trsm ? -panel[(r0 + rw + i) * kNC + cc] : 0.f;
+    {
+      const float4 b4 = *reinterpret_cast<const float4*>(pcol + r0 + rw);
+      v[0] = trsm ? -b4.x : 0.f;
+      v[1] = trsm ? -b4.y : 0.f;
+      v[2] = trsm ? -b4.z : 0.f;
+      v[3] = trsm ? -b4.w : 0.f;
+    }
     pack(v);
-    for (int J = 0; J < I; ++J) block_mma(panel + J * kRB * kNC);
+    for (int J = 0; J < I; ++J) block_mma(pcol + J * kRB);
     if (trsm) {
       // acc = -(b_I - sum L'X); X_I = (-inv(L'_II)) * acc
       unpack(v);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) cbuf[(rw + i) * kNC + cc] = v[i];
+      *reinterpret_cast<float4*>(ccol + rw) = make_float4(v[0], v[1], v[2], v[3]);
       named_sync(1, kThreads);
       acc[0] = acc[1] = 0ull;
-      block_mma(cbuf);
+      block_mma(ccol);
       unpack(v);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) panel[(r0 + rw + i) * kNC + cc] = v[i];
+      *reinterpret_cast<float4*>(pcol + r0 + rw) = make_float4(v[0], v[1], v[2], v[3]);
       named_sync(1, kThreads);  // X_I visible; cbuf free
     } else {
-      block_mma(panel + I * kRB * kNC);  // + L'_II * b_I
-      named_sync(1, kThreads);           // every warp has read b_I
+      block_mma(pcol + I * kRB);  // + L'_II * b_I
+      named_sync(1, kThreads);    // every warp has read b_I
       unpack(v);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) panel[(r0 + rw + i) * kNC + cc] = p.alpha * v[i];
+      *reinterpret_cast<float4*>(pcol + r0 + rw) =
+          make_float4(p.alpha * v[0], p.alpha * v[1], p.alpha * v[2], p.alpha * v[3]);
     }
   }
   named_sync(1, kThreads);
   for_panel([&](int r, int c, const float* g) {
-    if (r < n && c < ncols) *const_cast<float*>(g) = panel[r * kNC + c];
+    if (r < n && c < ncols) *const_cast<float*>(g) = panel[c * kPS + r];
   });
 }
 
 }  // namespace leaf32v3
 
-void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t s) {
+void launch_leaf32_pack_all(const LeafParams<float>& base, const long long* d_r0, const int* d_n, int nleaves,
+                            float* scratch, long long stride, cudaStream_t s) {
+  using namespace leaf32v3;
+  constexpr int kMaxBlk = kLeafMax / kRB;
+  dim3 grid(kMaxBlk * (kMaxBlk + 1) / 2, nleaves);
+  pack32_all_kernel<<<grid, 256, 0, s>>>(base, d_r0, d_n, scratch, stride);
+  ++launch_counter();
+}
+
+void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t s, bool prepacked) {
   using namespace leaf32v3;
   const int nblk = (p.n + kRB - 1) / kRB;
-  if (p.trsm || p.alpha != 0.f) {
+  if (!prepacked && (p.trsm || p.alpha != 0.f)) {
     pack32_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, scratch);
     ++launch_counter();
   }

@@ -463,6 +463,10 @@ int leaf_version() { return leaf64::leaf_version_env(); }
 
 void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s) {
   if (p.n <= 0 || p.nrhs <= 0) return;
+  if (p.packed) {  // triangle packed once for the whole recursion
+    launch_leaf_f32_v3(p, reinterpret_cast<float*>(p.packed), s, true);
+    return;
+  }
   double* P = nullptr;
   if (leaf64::leaf_version_env() >= 3) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;

@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
     // loads are complete: only now release the slot to the bulk-copy proxy.
     __syncwarp();
     if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads before the async refill
       mbar_arrive(empty0 + 8 * slot);
     }
     ++s;

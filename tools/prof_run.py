@@ -39,14 +39,16 @@ elif kind in ("gemm", "gemmtn", "sgemm", "tf32x3"):
     for i, x in enumerate((A, B, C)):
         rc.fill_uniform(x.view(), seed=i)
     rc.gemm(-1.0, ta, A.cview(), Trans.NoTrans, B.cview(), 1.0, C.view(), be)
-elif kind in ("leaf", "trmmleaf"):
+elif kind in ("leaf", "trmmleaf", "leaf32"):
     nb, m = args
+    if kind == "leaf32":
+        f64 = torch.float32
     A = MatrixBuffer(nb, nb, f64, "cuda")
     rc.fill_uniform(A.view(), seed=1)
     rc.make_dominant(A.view())
     B = MatrixBuffer(nb, m, f64, "cuda")
     rc.fill_uniform(B.view(), seed=2)
-    fn = rc.trsm_base if kind == "leaf" else rc.trmm_base
+    fn = rc.trmm_base if kind == "trmmleaf" else rc.trsm_base
     fn(TriangularSpec(), A.cview(), B.view(), nb, be)
 torch.cuda.synchronize()
 print("done", kind, args)
