@@ -456,7 +456,9 @@ int panel_streams(i64 rhs) {
   const char* e = getenv("RECTRI_CU_STREAMS");
   int p = e ? atoi(e) : 2;
   if (p > DeviceRes::kAux + 1) p = DeviceRes::kAux + 1;
-  while (p > 1 && rhs / p < 2048) --p;
+  const char* w = getenv("RECTRI_CU_PANEL_MIN");
+  const i64 min_w = w && atoll(w) > 0 ? atoll(w) : 2048;
+  while (p > 1 && rhs / p < min_w) --p;
   return p < 1 ? 1 : p;
 }
 

@@ -15,6 +15,14 @@
 //     lanes of a phase hit distinct bank pairs).
 // Accumulation is a k-ascending fma chain per element, independent of the
 // tile configuration.
+//
+// That is v1 (RECTRI_CU_SGEMM=1).  v2 (sgemm_ffma2_kernel, the default) keeps
+// the tile but stores every operand as [k][o] and double-buffers one k-step
+// of fragments in registers; see its comment.  B200, 8192x16384x8192:
+// NN 50.4 -> 52.8 TF/s, TN 41.1 -> 49.8, NT 53.7 -> 54.1 (FFMA peak 71).
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -232,6 +240,166 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
   }
 }
 
+// ---- v2: one shared layout for every transposition case.  k-contiguous
+// sources are transposed into [k][o] by 4-byte copies (lane -> 8 k x 4 o, so
+// a warp reads four 32-byte sectors and writes 32 distinct banks), so both
+// operands are read as two LDS.128 per k-step, one k-step of fragments is
+// double-buffered in registers across the k loop (and across tiles: the
+// next tile's first fragments are read right after its barrier), and every
+// case accumulates with FFMA2 on m-pairs.  Same k-ascending fma chain per
+// element as v1, so the two kernels agree bit for bit.
+template <int BO, int NT>
+struct TLoaderKC {
+  static constexpr int RS = BO + kPadMC;
+  static_assert(NT == 256 && BO % 32 == 0, "8 k x 32 o per pass");
+  const float* base;
+  const float* p0;
+  i64 step32;
+  int kl, ol, o_lim, k_lim;
+
+  __device__ void init(const float* X, i64 ld, i64 o0, i64 O, i64 K) {
+    kl = threadIdx.x % 8;
+    ol = threadIdx.x / 8;
+    o_lim = static_cast<int>(O - o0 < (1 << 30) ? O - o0 : (1 << 30));
+    k_lim = static_cast<int>(K < (1 << 30) ? K : (1 << 30));
+    base = X + o0 * ld;
+    p0 = base + static_cast<i64>(ol) * ld + kl;
+    step32 = 32 * ld;
+  }
+  __device__ __forceinline__ void load(float* s, i64 kt) const {
+    const int k0 = static_cast<int>(kt * kBK);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int ob = 0; ob < BO / 32; ++ob) {
+        const int k = kl + 8 * h, o = ol + 32 * ob;
+        const bool ok = k0 + k < k_lim && o < o_lim;
+        cp_async4(s + k * RS + o, ok ? p0 + ob * step32 + k0 + 8 * h : base, ok ? 4 : 0);
+      }
+  }
+};
+
+template <int BO>
+__device__ __forceinline__ void read_k(const float* s, int t, int k, float (&v)[8]) {
+  constexpr int RS = BO + kPadMC;
+  const float4 a = *reinterpret_cast<const float4*>(s + k * RS + 4 * t);
+  const float4 b = *reinterpret_cast<const float4*>(s + k * RS + BO / 2 + 4 * t);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB>
+__global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<float> p) {
+  constexpr int TX = 16, NT = 256;
+  static_assert(BM == 128 && BN == 128, "16 x 16 threads of 8 x 8");
+  constexpr bool A_KC = TA, B_KC = !TB;
+  constexpr int A_EL = kBK * (BM + kPadMC), B_EL = kBK * (BN + kPadMC);
+  using LA = std::conditional_t<A_KC, TLoaderKC<BM, NT>, FLoader<BM, NT, VA, false>>;
+  using LB = std::conditional_t<B_KC, TLoaderKC<BN, NT>, FLoader<BN, NT, VB, false>>;
+  extern __shared__ __align__(128) float fsmem[];
+  float* sA = fsmem;
+  float* sB = fsmem + STAGES * A_EL;
+
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const i64 m0 = static_cast<i64>(blockIdx.x) * BM;
+  const i64 n0 = static_cast<i64>(blockIdx.y) * BN;
+  const i64 KT = ceil_div(p.K, kBK);
+  LA la;
+  LB lb;
+  la.init(p.A, p.lda, m0, p.M, p.K);
+  lb.init(p.B, p.ldb, n0, p.N, p.K);
+
+  unsigned long long acc2[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc2[i][j] = 0ull;
+
+#pragma unroll
+  for (int s = 0; s < STAGES; ++s) {
+    if (s < KT) {
+      la.load(sA + s * A_EL, s);
+      lb.load(sB + s * B_EL, s);
+    }
+    cp_async_commit();
+  }
+  cp_async_wait<STAGES - 1>();
+  __syncthreads();
+  float fa[2][8], fb[2][8];
+  read_k<BM>(sA, ty, 0, fa[0]);
+  read_k<BN>(sB, tx, 0, fb[0]);
+  int st = 0;
+  for (i64 kt = 0; kt < KT; ++kt) {
+    const float* a_s = sA + st * A_EL;
+    const float* b_s = sB + st * B_EL;
+#pragma unroll
+    for (int k = 0; k < kBK; ++k) {
+      const int cb = k & 1;
+      if (k + 1 < kBK) {
+        read_k<BM>(a_s, ty, k + 1, fa[cb ^ 1]);
+        read_k<BN>(b_s, tx, k + 1, fb[cb ^ 1]);
+      } else {
+        // every thread has read tile kt: refill its stage, move to kt + 1
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        if (kt + STAGES < KT) {
+          la.load(sA + st * A_EL, kt + STAGES);
+          lb.load(sB + st * B_EL, kt + STAGES);
+        }
+        cp_async_commit();
+        st = st + 1 == STAGES ? 0 : st + 1;
+        if (kt + 1 < KT) {
+          read_k<BM>(sA + st * A_EL, ty, 0, fa[cb ^ 1]);
+          read_k<BN>(sB + st * B_EL, tx, 0, fb[cb ^ 1]);
+        }
+      }
+#pragma unroll
+      for (int ip = 0; ip < 4; ++ip) {
+        unsigned long long ap;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(ap) : "f"(fa[cb][2 * ip]), "f"(fa[cb][2 * ip + 1]));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          unsigned long long bb;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(bb) : "f"(fb[cb][j]));
+          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[ip][j]) : "l"(ap), "l"(bb));
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  const bool beta_zero = p.beta == 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const i64 n = n0 + FFrag<BN, false>::outer(tx, j);
+    if (n >= p.N) continue;
+    float accj[8], cold[8];
+#pragma unroll
+    for (int ip = 0; ip < 4; ++ip)
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(accj[2 * ip]), "=f"(accj[2 * ip + 1]) : "l"(acc2[ip][j]));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const i64 m = m0 + FFrag<BM, false>::outer(ty, i);
+      cold[i] = (!beta_zero && m < p.M) ? p.C[m + n * p.ldc] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const i64 m = m0 + FFrag<BM, false>::outer(ty, i);
+      if (m < p.M) p.C[m + n * p.ldc] = beta_zero ? p.alpha * accj[i] : fmaf(p.alpha, accj[i], p.beta * cold[i]);
+    }
+  }
+}
+
+template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB>
+void launch_cfg2(const GemmParams<float>& p, cudaStream_t s) {
+  auto kern = sgemm_ffma2_kernel<BM, BN, STAGES, TA, TB, VA, VB>;
+  constexpr int smem = STAGES * kBK * (BM + BN + 2 * kPadMC) * static_cast<int>(sizeof(float));
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
+  kern<<<grid, 256, smem, s>>>(p);
+  ++launch_counter();
+}
+
 template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB>
 void launch_cfg(const GemmParams<float>& p, cudaStream_t s) {
   auto kern = sgemm_ffma_kernel<BM, BN, STAGES, TA, TB, VA, VB>;
@@ -269,12 +437,39 @@ void dispatch(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
 #undef RECTRI_CFG
 }
 
+// v2: only outer-contiguous sources have a copy width (16-byte chunks when
+// 16-byte aligned); k-contiguous sources are always copied 4 bytes at a time.
+template <int BM, int BN, int STAGES>
+void dispatch2(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
+  const bool va = ta || (aligned(p.A, 16) && p.lda % 4 == 0);
+  const bool vb = !tb || (aligned(p.B, 16) && p.ldb % 4 == 0);
+#define RECTRI_CFG2(TA_, TB_)                                                             \
+  if (ta == TA_ && tb == TB_) {                                                           \
+    if (va && vb) launch_cfg2<BM, BN, STAGES, TA_, TB_, 4, 4>(p, s);                      \
+    else if (va) launch_cfg2<BM, BN, STAGES, TA_, TB_, 4, 1>(p, s);                       \
+    else if (vb) launch_cfg2<BM, BN, STAGES, TA_, TB_, 1, 4>(p, s);                       \
+    else launch_cfg2<BM, BN, STAGES, TA_, TB_, 1, 1>(p, s);                               \
+    return;                                                                               \
+  }
+  RECTRI_CFG2(false, false)
+  RECTRI_CFG2(true, false)
+  RECTRI_CFG2(false, true)
+  RECTRI_CFG2(true, true)
+#undef RECTRI_CFG2
+}
+
+int sgemm_version() {
+  const char* e = getenv("RECTRI_CU_SGEMM");
+  return e && atoi(e) == 1 ? 1 : 2;
+}
+
 }  // namespace
 
 void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
   if (tf32x3_enabled() && launch_gemm_f32_tf32x3(p, ta, tb, s)) return;
-  dispatch<128, 128, 3>(p, ta, tb, s);
+  if (sgemm_version() == 2) dispatch2<128, 128, 3>(p, ta, tb, s);
+  else dispatch<128, 128, 3>(p, ta, tb, s);
 }
 
 }  // namespace rectri_cu

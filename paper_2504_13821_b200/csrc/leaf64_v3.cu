@@ -37,13 +37,19 @@ namespace rectri_cu {
 namespace leaf64v3 {
 
 constexpr int kRB = 32;
-constexpr int kNC = 32;
 constexpr int kThreads = 256;
 constexpr int kBlk = kRB * kRB;
 constexpr int kMaxBlk = kLeafMax / kRB;
 constexpr size_t kScratchDoubles = static_cast<size_t>(kMaxBlk * (kMaxBlk + 1) / 2) * kBlk;
 
-__device__ __forceinline__ int panel_idx(int r, int c) { return swz64(r, c, kNC); }
+// Panel element (r, c) of an NC-wide panel: XOR-swizzled pairs for NC >= 16;
+// NC = 8 rows are 64 bytes and the B-fragment reads (4 rows x 8 columns)
+// are conflict-free unswizzled.
+template <int NC>
+__device__ __forceinline__ int panel_idx(int r, int c) {
+  if constexpr (NC >= 16) return swz64(r, c, NC);
+  else return r * NC + c;
+}
 
 __device__ __forceinline__ double lprime(const LeafParams<double>& p, int r, int j) {
   const int rr = p.reflected ? p.n - 1 - r : r;
@@ -141,7 +147,8 @@ __global__ void __launch_bounds__(256) pack3_all_kernel(const LeafParams<double>
 }
 
 constexpr int kRing = 5;  // packed blocks in flight (bulk copies)
-constexpr int kSmem = (kLeafMax * kNC + kRB * kNC + kRing * kBlk) * 8 + 2 * kRing * 8;
+template <int NC>
+constexpr int smem_bytes() { return (kLeafMax * NC + kRB * NC + kRing * kBlk) * 8 + 2 * kRing * 8; }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
@@ -174,8 +181,17 @@ __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 
+// NC right-hand sides per CTA (32, 16 or 8: narrower panels put more CTAs on
+// the SMs when the leaf has few right-hand sides).  The output tiles of a row
+// block (4 x NC/8 m8n8 tiles) go E per warp to CW compute warps; every
+// element's products are accumulated in the same order for every NC, so the
+// widths agree bit for bit.
+template <int NC>
 __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParams<double> p,
                                                                 const double* __restrict__ P) {
+  constexpr int kNC = NC;
+  constexpr int CW = NC >= 16 ? 8 : 4;           // compute warps
+  constexpr int E = 4 * (NC / 8) / CW;           // m8n8 tiles per compute warp
   extern __shared__ __align__(128) double smem3[];
   double* panel = smem3;                       // nb x 32 right-hand sides (swizzled rows)
   double* cbuf = smem3 + kLeafMax * kNC;       // TRSM: -(b_I - sum L'X) of the current row block
@@ -204,8 +220,9 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
         }
       }
     } else {
-      const int c = lane;
-      for (int r = warp; r < rows_p; r += kWarps) {
+      constexpr int RPW = 32 / kNC;  // rows per warp pass
+      const int c = lane % kNC;
+      for (int r = warp * RPW + lane / kNC; r < rows_p; r += kWarps * RPW) {
         const i64 sr = p.reflected ? n - 1 - r : r;
         f(r, c, p.B + sr * p.ldb + c0 + c);
       }
@@ -223,7 +240,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
   if (tid == 0) {
     for (int q = 0; q < kRing; ++q) {
       mbar_init(full0 + 8 * q, 1);
-      mbar_init(empty0 + 8 * q, kWarps);
+      mbar_init(empty0 + 8 * q, CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -241,30 +258,32 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
   }
   for_panel([&](int r, int c, const double* g) {
     const bool ok = r < n && c < ncols;
-    cp_async8(panel + panel_idx(r, c), ok ? g : p.B, ok ? 8 : 0);
+    cp_async8(panel + panel_idx<NC>(r, c), ok ? g : p.B, ok ? 8 : 0);
   });
   cp_async_commit();
 
   // warp w owns the m8n8 tiles (w & 3, 2*(w >> 2) + e), e = 0, 1.
   const int g = lane >> 2, t = lane & 3;
-  const int mt = warp & 3, nt0 = 2 * (warp >> 2);
+  const int mt = warp & 3, nt0 = E * (warp >> 2);
+  const bool computes = warp < CW;
   const uint32_t panel_u32 = smem_u32(panel), cbuf_u32 = smem_u32(cbuf);
-  uint32_t b_base[2];
+  uint32_t b_base[E];
 #pragma unroll
-  for (int e = 0; e < 2; ++e) b_base[e] = 8u * static_cast<uint32_t>(swz64(t, 8 * (nt0 + e) + g, kNC));
+  for (int e = 0; e < E; ++e) b_base[e] = 8u * static_cast<uint32_t>(panel_idx<NC>(t, 8 * (nt0 + e) + g));
   const uint32_t a_off = static_cast<uint32_t>((mt * 8 * 32 + lane) * 8);  // this lane's k-step-0 A fragment
   cp_async_wait<0>();
   named_sync(1, kThreads);  // panel loaded (GEMM warps only; the producer runs free)
   if (trsm && p.alpha != 1.0) {  // x = alpha * b (base_kernels.cpp:76-77)
-    for_panel([&](int r, int c, const double*) { panel[panel_idx(r, c)] *= p.alpha; });
+    for_panel([&](int r, int c, const double*) { panel[panel_idx<NC>(r, c)] *= p.alpha; });
     named_sync(1, kThreads);
   }
 
   // c[e][h] += A(block s) * Bsrc(32 rows at byte offset bsrc of a row-major
   // [k][kNC] swizzled buffer)
-  double c[2][2];
+  double c[E][2];
   int s = 0;
   auto block_mma = [&](uint32_t bsrc) {
+    if (!computes) return;
     const int slot = s % kRing;
     mbar_wait(full0 + 8 * slot, (s / kRing) & 1);
     const uint32_t as = smem_u32(ring + slot * kBlk) + a_off;
@@ -273,16 +292,16 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
     for (int kk = 0; kk < 8; ++kk)
       asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[kk]) : "r"(as + kk * 32 * 8));
     // all 8 k-steps' B fragments first: one shared-memory latency per block
-    double bv[kRB / 4][2];
+    double bv[kRB / 4][E];
 #pragma unroll
     for (int kk = 0; kk < kRB / 4; ++kk)
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
+      for (int e = 0; e < E; ++e)
         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(bv[kk][e]) : "r"(bsrc + b_base[e] + kk * 4 * kNC * 8));
 #pragma unroll
     for (int kk = 0; kk < kRB / 4; ++kk)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) dmma884(c[e][0], c[e][1], a[kk], bv[kk][e]);
+      for (int e = 0; e < E; ++e) dmma884(c[e][0], c[e][1], a[kk], bv[kk][e]);
     // The DMMAs have consumed every fragment loaded from the slot, so those
     // loads are complete: only now release the slot to the bulk-copy proxy.
     __syncwarp();
@@ -298,47 +317,64 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
     const int r0 = I * kRB;
     if (trsm) {
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
+      for (int e = 0; e < E; ++e)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) c[e][h] = -panel[panel_idx(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)];
+        for (int h = 0; h < 2; ++h) c[e][h] = !computes ? 0.0 : -panel[panel_idx<NC>(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)];
     } else {
-      c[0][0] = c[0][1] = c[1][0] = c[1][1] = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) c[e][0] = c[e][1] = 0.0;
     }
     for (int J = 0; J < I; ++J) block_mma(panel_u32 + static_cast<uint32_t>(J * kRB * kNC * 8));
     if (trsm) {
       // c = -(b_I - sum L'X); X_I = (-inv(L'_II)) * c
+      if (computes)
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
+      for (int e = 0; e < E; ++e)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) cbuf[panel_idx(8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
+        for (int h = 0; h < 2; ++h) cbuf[panel_idx<NC>(8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
       named_sync(1, kThreads);
-      c[0][0] = c[0][1] = c[1][0] = c[1][1] = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) c[e][0] = c[e][1] = 0.0;
       block_mma(cbuf_u32);
+      if (computes)
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
+      for (int e = 0; e < E; ++e)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) panel[panel_idx(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
+        for (int h = 0; h < 2; ++h) panel[panel_idx<NC>(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
       named_sync(1, kThreads);  // X_I visible; cbuf free
     } else {
       // c += L'_II * b_I; every warp reads b_I before anyone overwrites it
       block_mma(panel_u32 + static_cast<uint32_t>(I * kRB * kNC * 8));
       named_sync(1, kThreads);
+      if (computes)
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
+      for (int e = 0; e < E; ++e)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
-          panel[panel_idx(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = p.alpha * c[e][h];
+          panel[panel_idx<NC>(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = p.alpha * c[e][h];
     }
   }
   named_sync(1, kThreads);
   for_panel([&](int r, int cc, const double* gp) {
-    if (r < n && cc < ncols) *const_cast<double*>(gp) = panel[panel_idx(r, cc)];
+    if (r < n && cc < ncols) *const_cast<double*>(gp) = panel[panel_idx<NC>(r, cc)];
   });
 }
 
 }  // namespace leaf64v3
 
 size_t leaf3_scratch_doubles() { return leaf64v3::kScratchDoubles; }
+
+// Panel width for a leaf with nrhs right-hand sides: 32 while that still
+// gives two CTAs per SM, narrower when the leaf would leave SMs idle
+// (RECTRI_CU_LEAF_NC = 8 / 16 / 32 forces one).  Results do not depend on it.
+int leaf3_width(long long nrhs) {
+  const char* e = getenv("RECTRI_CU_LEAF_NC");
+  const int forced = e ? atoi(e) : 0;
+  if (forced == 8 || forced == 16 || forced == 32) return forced;
+  if (nrhs >= 32LL * 2 * 148) return 32;
+  if (nrhs > 1024) return 16;
+  return 8;
+}
 
 void launch_leaf3_pack_all(const LeafParams<double>& base, const long long* d_r0, const int* d_n, int nleaves,
                            double* scratch, cudaStream_t s) {
@@ -362,9 +398,14 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
     pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, scratch);
     ++launch_counter();
   }
-  const unsigned grid = static_cast<unsigned>(ceil_div(p.nrhs, kNC));
-  cudaFuncSetAttribute(leaf3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-  leaf3_kernel<<<grid, kThreads + 32, kSmem, s>>>(p, scratch);
+  const int nc = leaf3_width(p.nrhs);
+  auto go = [&](auto kern, int width, int smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), kThreads + 32, smem, s>>>(p, scratch);
+  };
+  if (nc == 32) go(leaf3_kernel<32>, 32, smem_bytes<32>());
+  else if (nc == 16) go(leaf3_kernel<16>, 16, smem_bytes<16>());
+  else go(leaf3_kernel<8>, 8, smem_bytes<8>());
   ++launch_counter();
 }
 

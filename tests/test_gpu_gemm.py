@@ -1,6 +1,8 @@
 """GPU GEMM update kernels (DMMA fp64 / FFMA fp32) through rectri_cu_gemm_*,
 against a float64 numpy reference -- test_gemm.cpp's cases plus odd shapes,
 strided subviews and every transpose form."""
+import itertools
+
 import numpy as np
 import pytest
 import torch
@@ -136,3 +138,29 @@ def test_tma_kernel_bitwise_equals_cp_async(cuda, ta, tb, monkeypatch):
             outs.append(to_np(C))
         for cfg, o in enumerate(outs[1:], 1):
             assert oracle.bitwise_equal(o, outs[0]), (M, N, K, cfg)
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_sgemm_v2_bitwise_equals_v1(cuda, ta, tb, monkeypatch):
+    """fp32 FFMA GEMM v2 (one [k][o] shared layout, transposing 4-byte copies,
+    FFMA2 for every case) against v1: the same k-ascending fma chain per
+    element, so identical bits -- ragged tails, sub-views at 4-byte offsets
+    (the 4-byte copy paths), alpha / beta including beta = 0."""
+    rng = np.random.default_rng(12)
+    for (M, N, K), (alpha, beta) in itertools.product(
+            ((130, 70, 50), (77, 129, 33), (200, 24, 1100), (128, 128, 16), (8, 8, 1), (257, 300, 129)),
+            ((-1.0, 1.0), (0.5, 0.0), (2.0, -0.25))):
+        for off in (0, 1):
+            a = F(rng.uniform(-1, 1, (K + 4, M + 2) if ta else (M + 4, K + 2)).astype(np.float32))
+            b = F(rng.uniform(-1, 1, (N + 2, K + 4) if tb else (K + 2, N + 4)).astype(np.float32))
+            c0 = F(rng.uniform(-1, 1, (M + 2, N)).astype(np.float32))
+            A, B = to_dev(a), to_dev(b)
+            av = A.cview().subview(off, 2, K, M) if ta else A.cview().subview(off, 2, M, K)
+            bv = B.cview().subview(off, 2, N, K) if tb else B.cview().subview(off, 2, K, N)
+            outs = []
+            for ver in ("1", "2"):
+                monkeypatch.setenv("RECTRI_CU_SGEMM", ver)
+                C = to_dev(c0)
+                gemm(alpha, Trans(ta), av, Trans(tb), bv, beta, C.view().subview(2, 0, M, N))
+                outs.append(to_np(C))
+            assert oracle.bitwise_equal(outs[0], outs[1]), (M, N, K, off, alpha, beta)

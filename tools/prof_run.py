@@ -1,6 +1,6 @@
 """One-shot workloads for ncu (never a bench number):
 
-    python tools/prof_run.py trsm N M T      one rec_trsm (direct launches)
+    python tools/prof_run.py trsm N M T      one rec_trsm (direct launches; strsm: fp32)
     python tools/prof_run.py gemm M N K      one DMMA GEMM update C -= A*B (NN)
     python tools/prof_run.py leaf NB M       one trsm_base leaf (NB x M)
 """
@@ -17,14 +17,16 @@ kind = sys.argv[1]
 args = [int(x) for x in sys.argv[2:]]
 f64 = torch.float64
 be = Backend.cuda(flags=NO_GRAPH)
-if kind in ("trsm", "trmm"):
+if kind in ("trsm", "trmm", "strsm"):
     n, m, t = args
+    if kind == "strsm":
+        f64 = torch.float32
     A = MatrixBuffer(n, n, f64, "cuda")
     rc.fill_uniform(A.view(), seed=1)
     rc.make_dominant(A.view())
     B = MatrixBuffer(n, m, f64, "cuda")
     rc.fill_uniform(B.view(), seed=2)
-    fn = rc.rec_trsm if kind == "trsm" else rc.rec_trmm
+    fn = rc.rec_trmm if kind == "trmm" else rc.rec_trsm
     fn(TriangularSpec(), A.cview(), B.view(), Threshold(t), be)
 elif kind in ("gemm", "gemmtn", "sgemm", "tf32x3"):
     M, N, K = args
