@@ -20,6 +20,20 @@ __global__ void scale_kernel(T* B, i64 ld, i64 rows, i64 cols, T alpha) {
   }
 }
 
+// D <- fma(c, S, D) over a rows x cols window (S packed, ld = rows): the
+// epilogue of a GEMM update with beta = 1, applied to a product that was
+// computed into S with alpha = 1, beta = 0 -- the same single rounding.
+template <typename T>
+__global__ void accumulate_kernel(T* D, i64 ldd, const T* S, i64 rows, i64 cols, T c) {
+  const i64 total = rows * cols;
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 col = i / rows, r = i - col * rows;
+    T* d = D + r + col * ldd;
+    *d = fma(c, S[i], *d);
+  }
+}
+
 template <typename T>
 __global__ void diag_zero_scan_kernel(const T* A, i64 lda, i64 n, uint8_t* flags) {
   for (i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; r < n;
@@ -49,6 +63,15 @@ void scale(T* B, i64 ld, i64 rows, i64 cols, T alpha, cudaStream_t s) {
 }
 
 template <typename T>
+void accumulate(T* D, i64 ldd, const T* S, i64 rows, i64 cols, T c, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  const i64 want = ceil_div(rows * cols, 256);
+  const unsigned grid = static_cast<unsigned>(want < 8 * sm_count() ? want : 8 * sm_count());
+  accumulate_kernel<T><<<grid, 256, 0, s>>>(D, ldd, S, rows, cols, c);
+  ++launch_counter();
+}
+
+template <typename T>
 void scan(const T* A, i64 lda, i64 n, uint8_t* flags, cudaStream_t s) {
   if (n <= 0) return;
   const unsigned grid = static_cast<unsigned>(ceil_div(n, 256) < sm_count() ? ceil_div(n, 256) : sm_count());
@@ -68,6 +91,12 @@ void launch_scale_f64(double* B, i64 ld, i64 rows, i64 cols, double alpha, cudaS
 }
 void launch_scale_f32(float* B, i64 ld, i64 rows, i64 cols, float alpha, cudaStream_t s) {
   scale<float>(B, ld, rows, cols, alpha, s);
+}
+void launch_accumulate_f64(double* D, i64 ldd, const double* S, i64 rows, i64 cols, double c, cudaStream_t s) {
+  accumulate<double>(D, ldd, S, rows, cols, c, s);
+}
+void launch_accumulate_f32(float* D, i64 ldd, const float* S, i64 rows, i64 cols, float c, cudaStream_t s) {
+  accumulate<float>(D, ldd, S, rows, cols, c, s);
 }
 void launch_diag_zero_scan_f64(const double* A, i64 lda, i64 n, uint8_t* flags, cudaStream_t s) {
   scan<double>(A, lda, n, flags, s);

@@ -207,6 +207,9 @@ struct K<double> {
   static void scale(double* B, i64 ld, i64 r, i64 c, double a, cudaStream_t s) {
     launch_scale_f64(B, ld, r, c, a, s);
   }
+  static void accumulate(double* D, i64 ldd, const double* S, i64 r, i64 c, double k, cudaStream_t s) {
+    launch_accumulate_f64(D, ldd, S, r, c, k, s);
+  }
   static void scan(const double* A, i64 lda, i64 n, uint8_t* f, cudaStream_t s) {
     launch_diag_zero_scan_f64(A, lda, n, f, s);
   }
@@ -219,6 +222,9 @@ struct K<float> {
   static void leaf(const LeafParams<float>& p, cudaStream_t s) { launch_leaf_f32(p, s); }
   static void scale(float* B, i64 ld, i64 r, i64 c, float a, cudaStream_t s) {
     launch_scale_f32(B, ld, r, c, a, s);
+  }
+  static void accumulate(float* D, i64 ldd, const float* S, i64 r, i64 c, float k, cudaStream_t s) {
+    launch_accumulate_f32(D, ldd, S, r, c, k, s);
   }
   static void scan(const float* A, i64 lda, i64 n, uint8_t* f, cudaStream_t s) {
     launch_diag_zero_scan_f32(A, lda, n, f, s);
@@ -299,6 +305,26 @@ struct KDesc {
   bool off_trans, off_on_left;
 };
 
+// Concurrent TRMM halves.  In a TRMM node the first half-problem writes the
+// GEMM's destination and the second overwrites the GEMM's source, so the
+// serial order is first -> GEMM -> second.  With a scratch S the GEMM can run
+// beside the first half: S = op(off) * src (alpha 1, beta 0: S is the exact
+// accumulator), then the second half on the GEMM's stream, and after the
+// join dst = fma(coeff, S, dst) -- the GEMM epilogue's own single rounding,
+// so the result is bitwise the serial one.  Used where the node's GEMM is
+// too small to fill the GPU (latency-bound small calls), with streams,
+// events and scratch from a per-call context; without one (or when it runs
+// out) nodes run serially.
+template <typename T>
+struct ConcCtx {
+  std::vector<cudaStream_t>* streams = nullptr;
+  std::vector<cudaEvent_t>* events = nullptr;
+  size_t next_stream = 0, next_event = 0;
+  T* scratch = nullptr;
+  i64 cap = 0, used = 0;
+  static constexpr i64 kMaxElems = i64(1) << 21;  // per node: mid x rhs
+};
+
 template <typename T>
 class Recursion {
  public:
@@ -317,6 +343,15 @@ class Recursion {
   double* packed = nullptr;
   size_t packed_stride = 0;
   int leaf_idx = 0;
+  ConcCtx<T>* conc = nullptr;
+
+  // Scratch elements the concurrent TRMM nodes of run(n, rhs) use.
+  static i64 conc_need(OpK op, i64 threshold, i64 n, i64 rhs) {
+    if (op != kTrmm || n <= threshold) return 0;
+    const i64 mid = n / 2, big = n - mid;
+    const i64 own = mid * rhs <= ConcCtx<T>::kMaxElems ? big * rhs : 0;
+    return own + conc_need(op, threshold, mid, rhs) + conc_need(op, threshold, big, rhs);
+  }
 
   // recursion.cpp:85-148
   void run(const Spec& spec, DView<const T> A, DView<T> B, i64 row0) {
@@ -341,12 +376,17 @@ class Recursion {
     const DView<T> b1 = left ? B.sub(0, 0, mid, B.cols) : B.sub(0, 0, B.rows, mid);
     const DView<T> b2 = left ? B.sub(mid, 0, n - mid, B.cols) : B.sub(0, mid, B.rows, n - mid);
 
-    if (sc.first_a22) run(spec, a22, b2, row0 + mid);
-    else run(spec, a11, b1, row0);
-
     const DView<T> dst = sc.write_b2 ? b2 : b1;
     const DView<const T> src = sc.read_b2 ? b2 : b1;
     const T coeff = static_cast<T>(sc.sign * (sc.carries_alpha ? spec.alpha : 1.0));
+    if (conc_node(sc, mid, rhs, dst)) {
+      run_concurrent(spec, sc, a11, a22, off, b1, b2, dst, src, coeff, mid, row0);
+      return;
+    }
+
+    if (sc.first_a22) run(spec, a22, b2, row0 + mid);
+    else run(spec, a11, b1, row0);
+
     emit(RECTRI_CU_EV_GEMM, dst.rows, dst.cols);
     if (before) before(false, off, sc.read_b2 ? b2 : b1, dst);
     if (kernels) {
@@ -362,6 +402,42 @@ class Recursion {
   }
 
  private:
+  bool conc_node(const Schema& sc, i64 mid, i64 rhs, DView<T> dst) {
+    if (!conc || dry_ || kernels || op_ != kTrmm || mid * rhs > ConcCtx<T>::kMaxElems) return false;
+    if (sc.first_a22 != sc.write_b2) return false;  // first half must be the GEMM's destination
+    return conc->next_stream < conc->streams->size() && conc->next_event + 2 <= conc->events->size() &&
+           conc->used + dst.rows * dst.cols <= conc->cap;
+  }
+
+  void run_concurrent(const Spec& spec, const Schema& sc, DView<const T> a11, DView<const T> a22,
+                      DView<const T> off, DView<T> b1, DView<T> b2, DView<T> dst, DView<const T> src,
+                      T coeff, i64 mid, i64 row0) {
+    cudaStream_t s2 = (*conc->streams)[conc->next_stream++];
+    cudaEvent_t fork = (*conc->events)[conc->next_event++];
+    cudaEvent_t join = (*conc->events)[conc->next_event++];
+    const DView<T> S{conc->scratch + conc->used, dst.rows, dst.rows, dst.cols};
+    conc->used += dst.rows * dst.cols;
+    cuda_check(cudaEventRecord(fork, s_), "record fork");
+    cuda_check(cudaStreamWaitEvent(s2, fork, 0), "wait fork");
+    // host call order (events, leaf numbering) is the serial one
+    if (sc.first_a22) run(spec, a22, b2, row0 + mid);
+    else run(spec, a11, b1, row0);
+    emit(RECTRI_CU_EV_GEMM, dst.rows, dst.cols);
+    if (before) before(false, off, sc.read_b2 ? b2 : b1, dst);
+    if (sc.off_on_left)
+      enqueue_gemm<T>(T(1), sc.off_trans != 0, off, false, src, T(0), S, s2);
+    else
+      enqueue_gemm<T>(T(1), false, src, sc.off_trans != 0, off, T(0), S, s2);
+    cudaStream_t s1 = s_;
+    s_ = s2;
+    if (sc.first_a22) run(spec, a11, b1, row0);
+    else run(spec, a22, b2, row0 + mid);
+    s_ = s1;
+    cuda_check(cudaEventRecord(join, s2), "record join");
+    cuda_check(cudaStreamWaitEvent(s_, join, 0), "wait join");
+    K<T>::accumulate(dst.p, dst.ld, S.p, dst.rows, dst.cols, coeff, s_);
+  }
+
   void emit(int32_t e, i64 n, i64 m) {
     if (events_) events_->push_back(Ev{e, n, m});
   }
@@ -431,6 +507,8 @@ struct DeviceRes {
   cudaStream_t capture = nullptr;
   cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr};
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the staged path
+  std::vector<cudaStream_t> conc_streams;     // concurrent TRMM nodes (ConcCtx)
+  std::vector<cudaEvent_t> conc_events;
   static constexpr int kSlots = 3;            // 0: A, 1..2: B panels
   void* stage[kSlots] = {nullptr, nullptr, nullptr};
   size_t stage_bytes[kSlots] = {0, 0, 0};
@@ -446,8 +524,18 @@ DeviceRes& device_res(int dev) {
     cuda_check(cudaStreamCreateWithFlags(&r.h2d, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking), "stream");
     for (auto& a : r.aux) cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
+    r.conc_streams.resize(16);
+    for (auto& a : r.conc_streams) cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
+    r.conc_events.resize(64);
+    for (auto& e : r.conc_events) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   }
   return r;
+}
+
+// Concurrent TRMM nodes (ConcCtx), on unless RECTRI_CU_TRMM_CONC=0.
+bool conc_enabled() {
+  const char* e = getenv("RECTRI_CU_TRMM_CONC");
+  return !(e && atoi(e) == 0);
 }
 
 // Streams the right-hand sides are split over (RECTRI_CU_STREAMS, default 2;
@@ -483,12 +571,14 @@ struct GraphEntry {
   uint8_t* h_flags = nullptr;
   double* packed = nullptr;  // fp64 leaf triangles, packed once per call
   void* leaf_meta = nullptr;  // their row offsets and orders
+  void* conc_scratch = nullptr;  // concurrent TRMM nodes' GEMM products
   i64 nodes = 0;
   int device = 0;
   ~GraphEntry() {
     if (exec) cudaGraphExecDestroy(exec);
     if (packed) cudaFree(packed);
     if (leaf_meta) cudaFree(leaf_meta);
+    if (conc_scratch) cudaFree(conc_scratch);
     if (d_flags) cudaFree(d_flags);
     if (h_flags) cudaFreeHost(h_flags);
   }
@@ -595,6 +685,34 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
       pbase.alpha = static_cast<T>(eff.alpha);
     }
   }
+  // Concurrent TRMM nodes (ConcCtx): packed leaves only (no per-stream leaf
+  // scratch), exact-FFMA fp32 only (3xTF32 keeps per-stream scratch).
+  ConcCtx<T> conc;
+  const bool left_ = spec.side == RECTRI_CU_LEFT;
+  const i64 rhs_ = left_ ? B.cols : B.rows;
+  const int P_ = g_prof.on ? 1 : panel_streams(rhs_);
+  // Only where the GPU is not already full: n <= 4096 (fp64) / 8192 (fp32).
+  const i64 conc_max_n = sizeof(T) == 8 ? 4096 : 8192;
+  if (op == kTrmm && nleaves > 0 && !g_prof.on && conc_enabled() && A.rows <= conc_max_n &&
+      !(std::is_same<T, float>::value && tf32x3_enabled())) {
+    const i64 w = P_ <= 1 ? rhs_ : ((rhs_ + P_ - 1) / P_ + 63) / 64 * 64;
+    i64 need = 0;
+    for (i64 r0 = 0; r0 < rhs_; r0 += w) need += Recursion<T>::conc_need(op, threshold, A.rows, std::min(w, rhs_ - r0));
+    if (need > 0 && need * static_cast<i64>(sizeof(T)) <= (i64(512) << 20)) {
+      DeviceRes* resp;
+      if (capture) {  // the capture path already holds g_mu
+        resp = &device_res(dev);
+      } else {
+        std::lock_guard<std::mutex> lock(g_mu);
+        resp = &device_res(dev);
+      }
+      cuda_check(cudaMalloc(&g->conc_scratch, static_cast<size_t>(need) * sizeof(T)), "trmm scratch alloc");
+      conc.streams = &resp->conc_streams;
+      conc.events = &resp->conc_events;
+      conc.scratch = static_cast<T*>(g->conc_scratch);
+      conc.cap = need;
+    }
+  }
   i64& counter = launch_counter();
   const i64 before = counter;
   if (capture) {
@@ -630,6 +748,7 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
       r.packed = g->packed;
       r.packed_stride = leaf3_scratch_doubles();
     }
+    if (conc.scratch) r.conc = &conc;
     return r;
   };
   if (scan) {

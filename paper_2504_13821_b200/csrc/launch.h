@@ -85,6 +85,8 @@ void launch_leaf32_pack_all(const LeafParams<float>& base, const long long* d_r0
 // B[rows x cols] (ld) <- alpha * B.
 void launch_scale_f64(double* B, i64 ld, i64 rows, i64 cols, double alpha, cudaStream_t s);
 void launch_scale_f32(float* B, i64 ld, i64 rows, i64 cols, float alpha, cudaStream_t s);
+void launch_accumulate_f64(double* D, i64 ldd, const double* S, i64 rows, i64 cols, double c, cudaStream_t s);
+void launch_accumulate_f32(float* D, i64 ldd, const float* S, i64 rows, i64 cols, float c, cudaStream_t s);
 // flags[r] = (A(r, r) == 0) for r < n.
 void launch_diag_zero_scan_f64(const double* A, i64 lda, i64 n, uint8_t* flags, cudaStream_t s);
 void launch_diag_zero_scan_f32(const float* A, i64 lda, i64 n, uint8_t* flags, cudaStream_t s);

@@ -378,3 +378,22 @@ def test_host_streamed_singular(cuda):
     with pytest.raises(SingularityError) as ei:
         rec_trsm(tspec(s), A.cview(), B.view(), Threshold(256))
     assert ei.value.index() == 1500
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_trmm_concurrent_halves_bitwise_serial(cuda, dt, monkeypatch):
+    """Small TRMM nodes run the first half beside the GEMM into a scratch
+    product and add it after the join (driver.cu ConcCtx): bitwise the
+    serial recursion (RECTRI_CU_TRMM_CONC=0) on every variant, alpha != 1,
+    graph and direct launches, several depths of concurrent nodes."""
+    for n, m, t in ((1000, 130, 64), (520, 40, 32)):
+        for s in oracle.all_variants(alpha=-1.25):
+            a = oracle.make_operand(s, False, n, 31, dt)
+            b = oracle.make_rhs(s, n, m, 32, dt)
+            monkeypatch.setenv("RECTRI_CU_TRMM_CONC", "0")
+            ser = run_op("trmm", s, a, b, t, backend=Backend.cuda(flags=NO_GRAPH))
+            monkeypatch.setenv("RECTRI_CU_TRMM_CONC", "1")
+            conc_graph = run_op("trmm", s, a, b, t)
+            conc_direct = run_op("trmm", s, a, b, t, backend=Backend.cuda(flags=NO_GRAPH))
+            assert oracle.bitwise_equal(ser, conc_graph), (n, s)
+            assert oracle.bitwise_equal(ser, conc_direct), (n, s)
