@@ -27,9 +27,6 @@ namespace rectri_cu {
 namespace leaf32v3 {
 
 constexpr int kRB = 32;
-constexpr int kNC = 32;
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
 constexpr int kBlk = kRB * kRB;  // floats per packed block
 constexpr int kRing = 8;
 // Panel and partial-result buffers are column-major per right-hand side
@@ -37,7 +34,8 @@ constexpr int kRing = 8;
 // column as one conflict-free ld.shared.v4 (bank = 4c + r mod 32).
 constexpr int kPS = kLeafMax + 4;  // panel column stride (floats)
 constexpr int kCS = kRB + 4;       // cbuf column stride
-constexpr int kSmem = (kNC * kPS + kNC * kCS + kRing * kBlk) * 4 + 2 * kRing * 8;
+template <int NC>
+constexpr int smem_bytes() { return (NC * kPS + NC * kCS + kRing * kBlk) * 4 + 2 * kRing * 8; }
 
 __device__ __forceinline__ float lprime(const LeafParams<float>& p, int r, int j) {
   const int rr = p.reflected ? p.n - 1 - r : r;
@@ -148,8 +146,16 @@ __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads + 32, 3) leaf32_kernel(const LeafParams<float> p,
-                                                                 const float* __restrict__ P) {
+// NC right-hand sides per CTA (32, 16 or 8): 8 row groups x NC columns of
+// compute threads (NC / 4 warps) plus the producer warp; each thread keeps
+// its 4 rows x 1 right-hand side and the same k order for every NC, so the
+// widths agree bit for bit.
+template <int NC>
+__global__ void __launch_bounds__(8 * NC + 32, NC == 32 ? 3 : 4) leaf32_kernel(const LeafParams<float> p,
+                                                            const float* __restrict__ P) {
+  constexpr int kNC = NC;
+  constexpr int kWarps = NC / 4;
+  constexpr int kThreads = kWarps * 32;
   extern __shared__ __align__(128) float smem32[];
   float* panel = smem32;                  // [c][r], stride kPS
   float* cbuf = panel + kNC * kPS;        // [c][r], stride kCS
@@ -179,8 +185,9 @@ __global__ void __launch_bounds__(kThreads + 32, 3) leaf32_kernel(const LeafPara
         }
       }
     } else {
-      const int c = lane;
-      for (int r = warp; r < rows_p; r += kWarps) {
+      constexpr int RPW = 32 / kNC;  // rows per warp pass
+      const int c = lane % kNC;
+      for (int r = warp * RPW + lane / kNC; r < rows_p; r += kWarps * RPW) {
         const i64 sr = p.reflected ? n - 1 - r : r;
         f(r, c, p.B + sr * p.ldb + c0 + c);
       }
@@ -226,8 +233,9 @@ __global__ void __launch_bounds__(kThreads + 32, 3) leaf32_kernel(const LeafPara
     named_sync(1, kThreads);
   }
 
-  // Thread (warp w, lane c): rows 4w .. 4w+3 of the row block, right-hand side c.
-  const int rw = 4 * warp, cc = lane;
+  // Thread (row group g, column c): rows 4g .. 4g+3 of the row block,
+  // right-hand side c (NC = 32: g = warp, c = lane).
+  const int rw = 4 * (warp * (32 / kNC) + lane / kNC), cc = lane % kNC;
   unsigned long long acc[2];  // packed pairs (rows 4w, 4w+1), (4w+2, 4w+3)
   int s = 0;
   // acc += block(s) * src(32 rows of column cc, consecutive floats)
@@ -325,9 +333,14 @@ void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t
     pack32_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, scratch);
     ++launch_counter();
   }
-  const unsigned grid = static_cast<unsigned>(ceil_div(p.nrhs, kNC));
-  cudaFuncSetAttribute(leaf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-  leaf32_kernel<<<grid, kThreads + 32, kSmem, s>>>(p, scratch);
+  auto go = [&](auto kern, int width, int smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), 8 * width + 32, smem, s>>>(p, scratch);
+  };
+  const int nc = leaf3_width(p.nrhs);
+  if (nc == 32) go(leaf32_kernel<32>, 32, smem_bytes<32>());
+  else if (nc == 16) go(leaf32_kernel<16>, 16, smem_bytes<16>());
+  else go(leaf32_kernel<8>, 8, smem_bytes<8>());
   ++launch_counter();
 }
 

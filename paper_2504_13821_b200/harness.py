@@ -9,8 +9,12 @@ headers of bench.hpp:64-67.  Differences, all deliberate:
 * backend is "cuda" (recorded as such in the `backend` column); "cublas"
   times cuBLAS ?trsm/?trmm on the same inputs through tools/libcublas_cmp.so
   so `ratio` can compare the two (Fig.-3-style reports);
-* timing uses CUDA events around each call (device time), inputs copied to
-  the device outside the timed region like the reference copies B;
+* timing uses CUDA events around each call, inputs copied to the device
+  outside the timed region like the reference copies B; the call is made
+  with RECTRI_CU_ASYNC and completed (singularity reported) by `sync()`
+  after the end event, so the events bracket enqueue + device time the same
+  way they bracket the cuBLAS call of the "cublas" backend (a synchronous
+  call would add the host's wake-up from the stream synchronize, ~14 us);
 * the residual gate also rejects non-finite results (the reference's gate
   passes inf because std::max drops NaN, SURVEY.md 8(d)).
 """
@@ -29,8 +33,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .api import (Backend, Diag, MatrixBuffer, OpKind, Side, Threshold, Trans, TriangularSpec, Uplo, effective_op,
-                  rec_trmm, rec_trsm, to_string, validate, variant_string)
+from .api import (ASYNC, Backend, Diag, MatrixBuffer, OpKind, Side, Threshold, Trans, TriangularSpec, Uplo, effective_op,
+                  rec_trmm, rec_trsm, sync, to_string, validate, variant_string)
 from .errors import ConfigError, IoError, JoinError, SingularityError, ValidationError
 
 SWEEP_CSV_HEADER = "op,variant,n,m,threshold,backend,elem,median_time_s,min_time_s,gflops"
@@ -205,8 +209,9 @@ def time_one(config: BenchConfig, n: int, m: int, seed: int) -> BenchRecord:
                 else:
                     fn = rec_trsm if config.op == OpKind.Trsm else rec_trmm
                     e0.record()
-                    fn(config.spec, A.cview(), B.view(), config.threshold, Backend.cuda())
+                    fn(config.spec, A.cview(), B.view(), config.threshold, Backend.cuda(flags=ASYNC))
                     e1.record()
+                    sync()
                     torch.cuda.synchronize()
                     ms = e0.elapsed_time(e1)
                 res = B.tensor()

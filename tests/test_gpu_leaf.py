@@ -107,16 +107,18 @@ def test_leaf32_v3_matches_v1_and_oracle(cuda, monkeypatch, op, side, uplo, tran
         assert float(np.max(np.abs(v3 - v1))) <= 64 * n * eps * scale, (n, m)
 
 
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
 @pytest.mark.parametrize("op", ["trsm", "trmm"])
 @pytest.mark.parametrize("side,uplo,trans,diag", VARIANTS)
-def test_leaf_v3_panel_widths_bitwise(cuda, monkeypatch, op, side, uplo, trans, diag):
-    """leaf3 with 8-, 16- and 32-wide right-hand-side panels (the width
-    follows the leaf's right-hand-side count): the same products in the same
-    order per element, so identical bits, ragged panels included."""
+def test_leaf_v3_panel_widths_bitwise(cuda, monkeypatch, dt, op, side, uplo, trans, diag):
+    """leaf3 / leaf32 with 8-, 16- and 32-wide right-hand-side panels (the
+    width follows the leaf's right-hand-side count): the same products in the
+    same order per element, so identical bits, ragged panels included."""
     rng = np.random.default_rng(500 + 8 * side + 4 * uplo + 2 * trans + diag)
     for n, m, alpha in ((33, 70, 1.0), (100, 13, -0.75), (256, 96, 1.0), (200, 41, 2.0)):
         s = oracle.spec(side, uplo, trans, diag, alpha)
         a, b = _inputs(op, s, n, m, rng)
+        a, b = F(a.astype(dt)), F(b.astype(dt))
         outs = []
         for nc in ("32", "16", "8"):
             monkeypatch.setenv("RECTRI_CU_LEAF_NC", nc)
