@@ -42,11 +42,11 @@ struct FLayout {
 // Per-thread loader.  MC: (o, k) at X[o + k*ld], chunks of VEC floats along
 // o into [k][o]; KC: (o, k) at X[k + o*ld], chunks of VEC floats along k into
 // [o][k].  The thread's chunk column is fixed, its row advances by STEP.
-template <int BO, int NT, int VEC, bool KC>
+template <int BO, int NT, int VEC, bool KC, int BKT = kBK>
 struct FLoader {
-  static constexpr int WIDTH = KC ? kBK : BO;  // source run length per row
+  static constexpr int WIDTH = KC ? BKT : BO;  // source run length per row
   static constexpr int CPR = WIDTH / VEC;
-  static constexpr int ROWS = KC ? BO : kBK;
+  static constexpr int ROWS = KC ? BO : BKT;
   static constexpr int IT = CPR * ROWS / NT;
   static constexpr int STEP = NT / CPR;
   static_assert(NT % CPR == 0 && (CPR * ROWS) % NT == 0, "loader trip count");
@@ -71,7 +71,7 @@ struct FLoader {
   }
 
   __device__ __forceinline__ void load(float* s, i64 kt) const {
-    const int k0 = static_cast<int>(kt * kBK);
+    const int k0 = static_cast<int>(kt * BKT);
     const float* tb = p0 + (KC ? static_cast<i64>(k0) : static_cast<i64>(k0) * ld);
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
 // next tile's first fragments are read right after its barrier), and every
 // case accumulates with FFMA2 on m-pairs.  Same k-ascending fma chain per
 // element as v1, so the two kernels agree bit for bit.
-template <int BO, int NT>
+template <int BO, int NT, int BK = kBK>
 struct TLoaderKC {
   static constexpr int RS = BO + kPadMC;
   static_assert(NT == 256 && BO % 32 == 0, "8 k x 32 o per pass");
@@ -267,9 +267,9 @@ struct TLoaderKC {
     step32 = 32 * ld;
   }
   __device__ __forceinline__ void load(float* s, i64 kt) const {
-    const int k0 = static_cast<int>(kt * kBK);
+    const int k0 = static_cast<int>(kt * BK);
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < BK / 8; ++h)
 #pragma unroll
       for (int ob = 0; ob < BO / 32; ++ob) {
         const int k = kl + 8 * h, o = ol + 32 * ob;
@@ -288,14 +288,14 @@ __device__ __forceinline__ void read_k(const float* s, int t, int k, float (&v)[
   v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
 
-template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB>
+template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB, int BK = kBK>
 __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<float> p) {
   constexpr int TX = 16, NT = 256;
   static_assert(BM == 128 && BN == 128, "16 x 16 threads of 8 x 8");
   constexpr bool A_KC = TA, B_KC = !TB;
-  constexpr int A_EL = kBK * (BM + kPadMC), B_EL = kBK * (BN + kPadMC);
-  using LA = std::conditional_t<A_KC, TLoaderKC<BM, NT>, FLoader<BM, NT, VA, false>>;
-  using LB = std::conditional_t<B_KC, TLoaderKC<BN, NT>, FLoader<BN, NT, VB, false>>;
+  constexpr int A_EL = BK * (BM + kPadMC), B_EL = BK * (BN + kPadMC);
+  using LA = std::conditional_t<A_KC, TLoaderKC<BM, NT, BK>, FLoader<BM, NT, VA, false, BK>>;
+  using LB = std::conditional_t<B_KC, TLoaderKC<BN, NT, BK>, FLoader<BN, NT, VB, false, BK>>;
   extern __shared__ __align__(128) float fsmem[];
   float* sA = fsmem;
   float* sB = fsmem + STAGES * A_EL;
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const i64 m0 = static_cast<i64>(blockIdx.x) * BM;
   const i64 n0 = static_cast<i64>(blockIdx.y) * BN;
-  const i64 KT = ceil_div(p.K, kBK);
+  const i64 KT = ceil_div(p.K, BK);
   LA la;
   LB lb;
   la.init(p.A, p.lda, m0, p.M, p.K);
@@ -333,9 +333,9 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
     const float* a_s = sA + st * A_EL;
     const float* b_s = sB + st * B_EL;
 #pragma unroll
-    for (int k = 0; k < kBK; ++k) {
+    for (int k = 0; k < BK; ++k) {
       const int cb = k & 1;
-      if (k + 1 < kBK) {
+      if (k + 1 < BK) {
         read_k<BM>(a_s, ty, k + 1, fa[cb ^ 1]);
         read_k<BN>(b_s, tx, k + 1, fb[cb ^ 1]);
       } else {
@@ -390,10 +390,10 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
   }
 }
 
-template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB>
+template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB, int BK = kBK>
 void launch_cfg2(const GemmParams<float>& p, cudaStream_t s) {
-  auto kern = sgemm_ffma2_kernel<BM, BN, STAGES, TA, TB, VA, VB>;
-  constexpr int smem = STAGES * kBK * (BM + BN + 2 * kPadMC) * static_cast<int>(sizeof(float));
+  auto kern = sgemm_ffma2_kernel<BM, BN, STAGES, TA, TB, VA, VB, BK>;
+  constexpr int smem = STAGES * BK * (BM + BN + 2 * kPadMC) * static_cast<int>(sizeof(float));
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
   kern<<<grid, 256, smem, s>>>(p);
@@ -439,16 +439,16 @@ void dispatch(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
 
 // v2: only outer-contiguous sources have a copy width (16-byte chunks when
 // 16-byte aligned); k-contiguous sources are always copied 4 bytes at a time.
-template <int BM, int BN, int STAGES>
+template <int BM, int BN, int STAGES, int BK = kBK>
 void dispatch2(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
   const bool va = ta || (aligned(p.A, 16) && p.lda % 4 == 0);
   const bool vb = !tb || (aligned(p.B, 16) && p.ldb % 4 == 0);
 #define RECTRI_CFG2(TA_, TB_)                                                             \
   if (ta == TA_ && tb == TB_) {                                                           \
-    if (va && vb) launch_cfg2<BM, BN, STAGES, TA_, TB_, 4, 4>(p, s);                      \
-    else if (va) launch_cfg2<BM, BN, STAGES, TA_, TB_, 4, 1>(p, s);                       \
-    else if (vb) launch_cfg2<BM, BN, STAGES, TA_, TB_, 1, 4>(p, s);                       \
-    else launch_cfg2<BM, BN, STAGES, TA_, TB_, 1, 1>(p, s);                               \
+    if (va && vb) launch_cfg2<BM, BN, STAGES, TA_, TB_, 4, 4, BK>(p, s);                  \
+    else if (va) launch_cfg2<BM, BN, STAGES, TA_, TB_, 4, 1, BK>(p, s);                   \
+    else if (vb) launch_cfg2<BM, BN, STAGES, TA_, TB_, 1, 4, BK>(p, s);                   \
+    else launch_cfg2<BM, BN, STAGES, TA_, TB_, 1, 1, BK>(p, s);                           \
     return;                                                                               \
   }
   RECTRI_CFG2(false, false)
@@ -468,7 +468,14 @@ int sgemm_version() {
 void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
   if (tf32x3_enabled() && launch_gemm_f32_tf32x3(p, ta, tb, s)) return;
-  if (sgemm_version() == 2) dispatch2<128, 128, 3>(p, ta, tb, s);
+  // k-tile depth: 32 for op-N A (fewer barriers; NN +2 %, NT +5 % at
+  // 8192x16384x8192), 16 for op-T A (two transposed operands at 32 spill).
+  // RECTRI_CU_SGEMM_BK = 16 / 32 forces one.  Results do not depend on it.
+  const char* e = getenv("RECTRI_CU_SGEMM_BK");
+  const int forced = e ? atoi(e) : 0;
+  const int bk = forced == 16 || forced == 32 ? forced : (ta ? 16 : 32);
+  if (sgemm_version() == 2 && bk == 32) dispatch2<128, 128, 3, 32>(p, ta, tb, s);
+  else if (sgemm_version() == 2) dispatch2<128, 128, 3>(p, ta, tb, s);
   else dispatch<128, 128, 3>(p, ta, tb, s);
 }
 

@@ -143,7 +143,7 @@ def test_tma_kernel_bitwise_equals_cp_async(cuda, ta, tb, monkeypatch):
 @pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
 def test_sgemm_v2_bitwise_equals_v1(cuda, ta, tb, monkeypatch):
     """fp32 FFMA GEMM v2 (one [k][o] shared layout, transposing 4-byte copies,
-    FFMA2 for every case) against v1: the same k-ascending fma chain per
+    FFMA2 for every case; 16- and 32-deep k-tiles) against v1: the same k-ascending fma chain per
     element, so identical bits -- ragged tails, sub-views at 4-byte offsets
     (the 4-byte copy paths), alpha / beta including beta = 0."""
     rng = np.random.default_rng(12)
@@ -158,9 +158,11 @@ def test_sgemm_v2_bitwise_equals_v1(cuda, ta, tb, monkeypatch):
             av = A.cview().subview(off, 2, K, M) if ta else A.cview().subview(off, 2, M, K)
             bv = B.cview().subview(off, 2, N, K) if tb else B.cview().subview(off, 2, K, N)
             outs = []
-            for ver in ("1", "2"):
+            for ver, bk in (("1", "16"), ("2", "16"), ("2", "32")):
                 monkeypatch.setenv("RECTRI_CU_SGEMM", ver)
+                monkeypatch.setenv("RECTRI_CU_SGEMM_BK", bk)
                 C = to_dev(c0)
                 gemm(alpha, Trans(ta), av, Trans(tb), bv, beta, C.view().subview(2, 0, M, N))
                 outs.append(to_np(C))
             assert oracle.bitwise_equal(outs[0], outs[1]), (M, N, K, off, alpha, beta)
+            assert oracle.bitwise_equal(outs[0], outs[2]), (M, N, K, off, alpha, beta, "bk32")
