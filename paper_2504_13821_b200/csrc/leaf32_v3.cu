@@ -147,15 +147,17 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 }
 
 // NC right-hand sides per CTA (32, 16 or 8): 8 row groups x NC columns of
-// compute threads (NC / 4 warps) plus the producer warp; each thread keeps
-// its 4 rows x 1 right-hand side and the same k order for every NC, so the
-// widths agree bit for bit.
+// compute threads as 8 row groups x NC/2 column pairs (NC / 8 warps) plus the
+// producer warp; each thread keeps 4 rows x 2 right-hand sides (one A read
+// feeds both columns) and the same k order for every NC, so the widths
+// agree bit for bit.
 template <int NC>
-__global__ void __launch_bounds__(8 * NC + 32, NC == 32 ? 3 : 4) leaf32_kernel(const LeafParams<float> p,
-                                                            const float* __restrict__ P) {
+__global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams<float> p,
+                                                                const float* __restrict__ P) {
   constexpr int kNC = NC;
-  constexpr int kWarps = NC / 4;
+  constexpr int kWarps = NC / 8;
   constexpr int kThreads = kWarps * 32;
+  constexpr int kCP = NC / 2;  // column pairs
   extern __shared__ __align__(128) float smem32[];
   float* panel = smem32;                  // [c][r], stride kPS
   float* cbuf = panel + kNC * kPS;        // [c][r], stride kCS
@@ -233,29 +235,36 @@ __global__ void __launch_bounds__(8 * NC + 32, NC == 32 ? 3 : 4) leaf32_kernel(c
     named_sync(1, kThreads);
   }
 
-  // Thread (row group g, column c): rows 4g .. 4g+3 of the row block,
-  // right-hand side c (NC = 32: g = warp, c = lane).
-  const int rw = 4 * (warp * (32 / kNC) + lane / kNC), cc = lane % kNC;
-  unsigned long long acc[2];  // packed pairs (rows 4w, 4w+1), (4w+2, 4w+3)
+  // Thread (row group g, column pair q): rows 4g .. 4g+3 of the row block,
+  // right-hand sides q and q + NC/2 (lanes: q fastest, so a warp's x reads
+  // hit consecutive columns -- 8 distinct bank groups per 8 lanes).
+  const int tq = warp * 32 + lane;
+  const int rw = 4 * (tq / kCP), cc = tq % kCP;
+  unsigned long long acc[2][2];  // [column][row pair]: (4g, 4g+1), (4g+2, 4g+3)
   int s = 0;
-  // acc += block(s) * src(32 rows of column cc, consecutive floats)
-  auto block_mma = [&](const float* src) {
+  // acc[j] += block(s) * src_j (32 consecutive rows of column j)
+  auto block_mma = [&](const float* src0, const float* src1) {
     const int slot = s % kRing;
     mbar_wait(full0 + 8 * slot, (s / kRing) & 1);
     const float* blk = ring + slot * kBlk;
 #pragma unroll
     for (int kb = 0; kb < kRB; kb += 4) {
-      const float4 x4 = *reinterpret_cast<const float4*>(src + kb);
-      const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+      const float4 x0 = *reinterpret_cast<const float4*>(src0 + kb);
+      const float4 x1 = *reinterpret_cast<const float4*>(src1 + kb);
+      const float xs[2][4] = {{x0.x, x0.y, x0.z, x0.w}, {x1.x, x1.y, x1.z, x1.w}};
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const float4 a = *reinterpret_cast<const float4*>(blk + (kb + kk) * kRB + rw);  // broadcast
-        unsigned long long a01, a23, xx;
+        unsigned long long a01, a23;
         asm("mov.b64 %0, {%1, %2};" : "=l"(a01) : "f"(a.x), "f"(a.y));
         asm("mov.b64 %0, {%1, %2};" : "=l"(a23) : "f"(a.z), "f"(a.w));
-        asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(xs[kk]));
-        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[0]) : "l"(a01), "l"(xx));
-        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[1]) : "l"(a23), "l"(xx));
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          unsigned long long xx;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(xs[j][kk]));
+          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[j][0]) : "l"(a01), "l"(xx));
+          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[j][1]) : "l"(a23), "l"(xx));
+        }
       }
     }
     // every fragment read from the slot has been consumed by an FFMA2 above;
@@ -267,46 +276,55 @@ __global__ void __launch_bounds__(8 * NC + 32, NC == 32 ? 3 : 4) leaf32_kernel(c
     }
     ++s;
   };
-  auto unpack = [&](float (&v)[4]) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(acc[0]));
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(acc[1]));
+  auto unpack = [&](int j, float (&v)[4]) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(acc[j][0]));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(acc[j][1]));
   };
-  auto pack = [&](const float (&v)[4]) {
-    asm("mov.b64 %0, {%1, %2};" : "=l"(acc[0]) : "f"(v[0]), "f"(v[1]));
-    asm("mov.b64 %0, {%1, %2};" : "=l"(acc[1]) : "f"(v[2]), "f"(v[3]));
+  auto pack = [&](int j, const float (&v)[4]) {
+    asm("mov.b64 %0, {%1, %2};" : "=l"(acc[j][0]) : "f"(v[0]), "f"(v[1]));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(acc[j][1]) : "f"(v[2]), "f"(v[3]));
   };
 
-  float* pcol = panel + cc * kPS;  // this lane's right-hand side, rows contiguous
-  float* ccol = cbuf + cc * kCS;
+  float* pcol[2] = {panel + cc * kPS, panel + (cc + kCP) * kPS};  // rows contiguous
+  float* ccol[2] = {cbuf + cc * kCS, cbuf + (cc + kCP) * kCS};
   for (int bi = 0; bi < nblk; ++bi) {
     const int I = trsm ? bi : nblk - 1 - bi;
     const int r0 = I * kRB;
-    float v[4];
-    {
-      const float4 b4 = *reinterpret_cast<const float4*>(pcol + r0 + rw);
-      v[0] = trsm ? -b4.x : 0.f;
-      v[1] = trsm ? -b4.y : 0.f;
-      v[2] = trsm ? -b4.z : 0.f;
-      v[3] = trsm ? -b4.w : 0.f;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float4 b4 = *reinterpret_cast<const float4*>(pcol[j] + r0 + rw);
+      const float v[4] = {trsm ? -b4.x : 0.f, trsm ? -b4.y : 0.f, trsm ? -b4.z : 0.f, trsm ? -b4.w : 0.f};
+      pack(j, v);
     }
-    pack(v);
-    for (int J = 0; J < I; ++J) block_mma(pcol + J * kRB);
+    for (int J = 0; J < I; ++J) block_mma(pcol[0] + J * kRB, pcol[1] + J * kRB);
     if (trsm) {
       // acc = -(b_I - sum L'X); X_I = (-inv(L'_II)) * acc
-      unpack(v);
-      *reinterpret_cast<float4*>(ccol + rw) = make_float4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float v[4];
+        unpack(j, v);
+        *reinterpret_cast<float4*>(ccol[j] + rw) = make_float4(v[0], v[1], v[2], v[3]);
+        acc[j][0] = acc[j][1] = 0ull;
+      }
       named_sync(1, kThreads);
-      acc[0] = acc[1] = 0ull;
-      block_mma(ccol);
-      unpack(v);
-      *reinterpret_cast<float4*>(pcol + r0 + rw) = make_float4(v[0], v[1], v[2], v[3]);
+      block_mma(ccol[0], ccol[1]);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float v[4];
+        unpack(j, v);
+        *reinterpret_cast<float4*>(pcol[j] + r0 + rw) = make_float4(v[0], v[1], v[2], v[3]);
+      }
       named_sync(1, kThreads);  // X_I visible; cbuf free
     } else {
-      block_mma(pcol + I * kRB);  // + L'_II * b_I
-      named_sync(1, kThreads);    // every warp has read b_I
-      unpack(v);
-      *reinterpret_cast<float4*>(pcol + r0 + rw) =
-          make_float4(p.alpha * v[0], p.alpha * v[1], p.alpha * v[2], p.alpha * v[3]);
+      block_mma(pcol[0] + I * kRB, pcol[1] + I * kRB);  // + L'_II * b_I
+      named_sync(1, kThreads);                         // every warp has read b_I
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float v[4];
+        unpack(j, v);
+        *reinterpret_cast<float4*>(pcol[j] + r0 + rw) =
+            make_float4(p.alpha * v[0], p.alpha * v[1], p.alpha * v[2], p.alpha * v[3]);
+      }
     }
   }
   named_sync(1, kThreads);
@@ -335,7 +353,7 @@ void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t
   }
   auto go = [&](auto kern, int width, int smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), 8 * width + 32, smem, s>>>(p, scratch);
+    kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), 4 * width + 32, smem, s>>>(p, scratch);
   };
   const int nc = leaf3_width(p.nrhs);
   if (nc == 32) go(leaf32_kernel<32>, 32, smem_bytes<32>());
