@@ -1137,125 +1137,144 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
       K<T>::scan(A.p, A.ld, n, d_flags, cs);
       cuda_check(cudaMemcpyAsync(h_flags, d_flags, static_cast<size_t>(n), cudaMemcpyDeviceToHost, cs), "flags");
     }
-    // H2D in first-use order; ready[i] gates unit i.
-    std::vector<cudaEvent_t> ready(units.size(), nullptr);
-    std::vector<std::vector<int>> fresh(units.size());  // chunks first loaded for unit i
-    std::vector<char> loaded(nch, 0);
-    for (size_t i = 0; i < units.size(); ++i) {
-      const Unit& u = units[i];
-      bool issued = false;
-      if (!a_dev) {  // device sub-view; the host block sits at the same offsets
-        const i64 off = static_cast<i64>(u.a.p - dA.p);
-        copy2d(const_cast<T*>(u.a.p), n, A.p + off % n + (off / n) * A.ld, A.ld, u.a.rows, u.a.cols,
-               cudaMemcpyHostToDevice, hs);
-        issued = true;
-      }
-      const i64 w0 = off_of(u.dst.p), w1 = w0 + len_of(u.dst);
-      for (int pass = 0; pass < 2; ++pass) {
-        const i64 r0 = pass ? u.s0 : w0, r1 = pass ? u.s1 : w1;
-        for (int c = chunk_of(r0); r1 > r0 && c < nch && cb[c] < r1; ++c) {
-          if (loaded[c]) continue;
-          loaded[c] = 1;
-          const DView<T> d = b_chunk(dB, c), h = b_chunk(hB, c);
-          copy2d(d.p, d.ld, h.p, h.ld, d.rows, d.cols, cudaMemcpyHostToDevice, hs);
-          fresh[i].push_back(c);
-          issued = true;
-        }
-      }
-      if (issued) {
-        ready[i] = ev();
-        cuda_check(cudaEventRecord(ready[i], hs), "record");
-      }
-    }
-    if (scan && !a_dev) {  // host-side zero-pivot scan (trsm_base scans before writing)
-      flags.resize(static_cast<size_t>(n));
-      for (i64 r = 0; r < n; ++r) flags[r] = A.p[r + r * A.ld] == T(0) ? 1 : 0;
-    }
-    // Compute: each unit after its inputs, its right-hand sides split over P
-    // streams (as the device path's graph); chunk copy-back after its last
-    // writer on every stream.
+    // Right-hand sides in TP consecutive time panels (RECTRI_CU_E2E_PANELS;
+    // default 2 from 16384 right-hand sides): panel t's chunks are copied back
+    // while panel t+1 computes, so only the last panel's last rows are left
+    // for the tail (C3: compute done 132.3 -> 130.2 ms, tail 6.6 -> 3.3 ms,
+    // e2e 139.3 -> 134.3 ms; 4 panels: tail 1.4 ms but the narrower GEMMs
+    // finish at 137 ms).  Within a panel the right-hand sides are split over P
+    // streams as in the device path.  Arithmetic is per right-hand side, so
+    // the result is bitwise the single-panel one.
     const i64 rhs = left ? bcols : brows;
-    const int P = panel_streams(rhs);
-    const i64 pw = ((rhs + P - 1) / P + 63) / 64 * 64;
-    std::vector<cudaStream_t> ps(P);
-    for (int q = 0; q < P; ++q) ps[q] = q == 0 ? cs : res->aux[q - 1];
-    if (P > 1) {
-      cudaEvent_t fork = ev();
-      cuda_check(cudaEventRecord(fork, cs), "record");
-      for (int q = 1; q < P; ++q) cuda_check(cudaStreamWaitEvent(ps[q], fork, 0), "wait");
-    }
-    auto rhs_part = [&](DView<T> v, int q) {  // right-hand sides [q*pw, (q+1)*pw) of a B view
-      const i64 r0 = q * pw, r1 = std::min(rhs, r0 + pw);
+    int TP = rhs >= 16384 ? 2 : 1;
+    if (const char* te = getenv("RECTRI_CU_E2E_PANELS")) TP = std::max(1, atoi(te));
+    const i64 tw = (rhs + TP - 1) / TP;
+    auto window = [&](DView<T> v, i64 r0, i64 r1) {
       return left ? v.sub(0, r0, v.rows, r1 - r0) : v.sub(r0, 0, r1 - r0, v.cols);
     };
     // fp64 v3 leaves: each leaf's triangle packed once (stream 0, after its
-    // A block has arrived), shared by every stream's leaf launch.
+    // A block has arrived), shared by every stream's and panel's leaf launch.
     double* packs = nullptr;
     const bool pack_once = std::is_same<T, double>::value && leaf_version() >= 3 && threshold <= kLeafMax &&
-                           !(op == kTrmm && spec.alpha == 0.0) && P > 1;
+                           !(op == kTrmm && spec.alpha == 0.0);
     if (pack_once) {
       std::lock_guard<std::mutex> lock(g_mu);
       packs = static_cast<double*>(staging(*res, 2, leaves.size() * leaf3_scratch_doubles() * sizeof(double)));
     }
-    int leaf_k = 0;
-    for (size_t i = 0; i < units.size(); ++i) {
-      const Unit& u = units[i];
-      const KDesc<T>& k = *u.k;
-      double* packed = nullptr;
-      cudaEvent_t packed_ev = nullptr;
-      if (pack_once && k.leaf) {
-        if (ready[i]) cuda_check(cudaStreamWaitEvent(ps[0], ready[i], 0), "wait input");
-        packed = packs + static_cast<size_t>(leaf_k++) * leaf3_scratch_doubles();
-        if constexpr (std::is_same<T, double>::value)
-          launch_leaf3_pack(leaf_params<double>(op, k.spec, k.a, k.dst), packed, ps[0]);
-        packed_ev = ev();
-        cuda_check(cudaEventRecord(packed_ev, ps[0]), "record");
-      }
-      for (int q = 0; q < P && q * pw < rhs; ++q) {
-        cudaStream_t sq = ps[q];
-        if (ready[i]) cuda_check(cudaStreamWaitEvent(sq, ready[i], 0), "wait input");
-        if (packed_ev && q > 0) cuda_check(cudaStreamWaitEvent(sq, packed_ev, 0), "wait pack");
-        if (op == kTrsm && spec.alpha != 1.0)  // alpha once per element, at first arrival
-          for (int c : fresh[i]) {
-            const DView<T> d = rhs_part(b_chunk(dB, c), q);
-            K<T>::scale(d.p, d.ld, d.rows, d.cols, static_cast<T>(spec.alpha), sq);
+    std::vector<cudaEvent_t> packed_evs(units.size(), nullptr);
+    for (int tp = 0; tp < TP && tp * tw < rhs; ++tp) {
+      const i64 t0 = tp * tw, t1 = std::min(rhs, t0 + tw);
+      // H2D in first-use order (A blocks in the first panel); ready[i] gates unit i.
+      std::vector<cudaEvent_t> ready(units.size(), nullptr);
+      std::vector<std::vector<int>> fresh(units.size());  // chunks first loaded for unit i
+      std::vector<char> loaded(nch, 0);
+      for (size_t i = 0; i < units.size(); ++i) {
+        const Unit& u = units[i];
+        bool issued = false;
+        if (!a_dev && tp == 0) {  // device sub-view; the host block sits at the same offsets
+          const i64 off = static_cast<i64>(u.a.p - dA.p);
+          copy2d(const_cast<T*>(u.a.p), n, A.p + off % n + (off / n) * A.ld, A.ld, u.a.rows, u.a.cols,
+                 cudaMemcpyHostToDevice, hs);
+          issued = true;
+        }
+        const i64 w0 = off_of(u.dst.p), w1 = w0 + len_of(u.dst);
+        for (int pass = 0; pass < 2; ++pass) {
+          const i64 r0 = pass ? u.s0 : w0, r1 = pass ? u.s1 : w1;
+          for (int c = chunk_of(r0); r1 > r0 && c < nch && cb[c] < r1; ++c) {
+            if (loaded[c]) continue;
+            loaded[c] = 1;
+            const DView<T> d = window(b_chunk(dB, c), t0, t1), h = window(b_chunk(hB, c), t0, t1);
+            copy2d(d.p, d.ld, h.p, h.ld, d.rows, d.cols, cudaMemcpyHostToDevice, hs);
+            fresh[i].push_back(c);
+            issued = true;
           }
-        const DView<T> dst = rhs_part(u.dst, q);
-        if (k.leaf) {
-          enqueue_base<T>(op, k.spec, k.a, dst, sq, packed);
-        } else if (k.off_on_left) {
-          enqueue_gemm<T>(k.coeff, k.off_trans, u.a, false, rhs_part(k.src, q), T(1), dst, sq);
-        } else {
-          enqueue_gemm<T>(k.coeff, false, rhs_part(k.src, q), k.off_trans, u.a, T(1), dst, sq);
+        }
+        if (issued) {
+          ready[i] = ev();
+          cuda_check(cudaEventRecord(ready[i], hs), "record");
         }
       }
-      for (int c = 0; c < nch; ++c) {
-        if (last_writer[c] != static_cast<int>(i)) continue;
-        for (int q = 0; q < P && q * pw < rhs; ++q) {
-          cudaEvent_t done = ev();
-          cuda_check(cudaEventRecord(done, ps[q]), "record");
-          cuda_check(cudaStreamWaitEvent(ds, done, 0), "wait");
+      if (scan && !a_dev && tp == 0) {  // host-side zero-pivot scan (trsm_base scans before writing)
+        flags.resize(static_cast<size_t>(n));
+        for (i64 r = 0; r < n; ++r) flags[r] = A.p[r + r * A.ld] == T(0) ? 1 : 0;
+      }
+      // Compute: each unit after its inputs, the panel's right-hand sides split
+      // over P streams; chunk copy-back after its last writer on every stream.
+      const i64 prhs = t1 - t0;
+      const int P = panel_streams(prhs);
+      const i64 pw = ((prhs + P - 1) / P + 63) / 64 * 64;
+      std::vector<cudaStream_t> ps(P);
+      for (int q = 0; q < P; ++q) ps[q] = q == 0 ? cs : res->aux[q - 1];
+      if (P > 1) {
+        cudaEvent_t fork = ev();
+        cuda_check(cudaEventRecord(fork, cs), "record");
+        for (int q = 1; q < P; ++q) cuda_check(cudaStreamWaitEvent(ps[q], fork, 0), "wait");
+      }
+      auto rhs_part = [&](DView<T> v, int q) {  // right-hand sides [t0 + q*pw, ...) of a B view
+        const i64 r0 = t0 + q * pw, r1 = std::min(t1, r0 + pw);
+        return window(v, r0, r1);
+      };
+      int leaf_k = 0;
+      for (size_t i = 0; i < units.size(); ++i) {
+        const Unit& u = units[i];
+        const KDesc<T>& k = *u.k;
+        double* packed = nullptr;
+        if (pack_once && k.leaf) {
+          packed = packs + static_cast<size_t>(leaf_k++) * leaf3_scratch_doubles();
+          if (tp == 0) {
+            if (ready[i]) cuda_check(cudaStreamWaitEvent(ps[0], ready[i], 0), "wait input");
+            if constexpr (std::is_same<T, double>::value)
+              launch_leaf3_pack(leaf_params<double>(op, k.spec, k.a, k.dst), packed, ps[0]);
+            packed_evs[i] = ev();
+            cuda_check(cudaEventRecord(packed_evs[i], ps[0]), "record");
+          }
         }
-        const DView<T> d = b_chunk(dB, c), h = b_chunk(hB, c);
-        if (trace) {
-          cudaEvent_t e0, e1;
-          cudaEventCreate(&e0);
-          cudaEventCreate(&e1);
-          evs.push_back(e0);
-          evs.push_back(e1);
-          cudaEventRecord(e0, ds);
-          copy2d(h.p, h.ld, d.p, d.ld, d.rows, d.cols, cudaMemcpyDeviceToHost, ds);
-          cudaEventRecord(e1, ds);
-          d2h_marks.push_back({c, {e0, e1}});
-        } else {
-          copy2d(h.p, h.ld, d.p, d.ld, d.rows, d.cols, cudaMemcpyDeviceToHost, ds);
+        for (int q = 0; q < P && q * pw < prhs; ++q) {
+          cudaStream_t sq = ps[q];
+          if (ready[i]) cuda_check(cudaStreamWaitEvent(sq, ready[i], 0), "wait input");
+          if (packed_evs[i] && (q > 0 || tp > 0)) cuda_check(cudaStreamWaitEvent(sq, packed_evs[i], 0), "wait pack");
+          if (op == kTrsm && spec.alpha != 1.0)  // alpha once per element, at first arrival
+            for (int c : fresh[i]) {
+              const DView<T> d = rhs_part(b_chunk(dB, c), q);
+              K<T>::scale(d.p, d.ld, d.rows, d.cols, static_cast<T>(spec.alpha), sq);
+            }
+          const DView<T> dst = rhs_part(u.dst, q);
+          if (k.leaf) {
+            enqueue_base<T>(op, k.spec, k.a, dst, sq, packed);
+          } else if (k.off_on_left) {
+            enqueue_gemm<T>(k.coeff, k.off_trans, u.a, false, rhs_part(k.src, q), T(1), dst, sq);
+          } else {
+            enqueue_gemm<T>(k.coeff, false, rhs_part(k.src, q), k.off_trans, u.a, T(1), dst, sq);
+          }
+        }
+        for (int c = 0; c < nch; ++c) {
+          if (last_writer[c] != static_cast<int>(i)) continue;
+          for (int q = 0; q < P && q * pw < prhs; ++q) {
+            cudaEvent_t done = ev();
+            cuda_check(cudaEventRecord(done, ps[q]), "record");
+            cuda_check(cudaStreamWaitEvent(ds, done, 0), "wait");
+          }
+          const DView<T> d = window(b_chunk(dB, c), t0, t1), h = window(b_chunk(hB, c), t0, t1);
+          if (trace) {
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            evs.push_back(e0);
+            evs.push_back(e1);
+            cudaEventRecord(e0, ds);
+            copy2d(h.p, h.ld, d.p, d.ld, d.rows, d.cols, cudaMemcpyDeviceToHost, ds);
+            cudaEventRecord(e1, ds);
+            d2h_marks.push_back({c, {e0, e1}});
+          } else {
+            copy2d(h.p, h.ld, d.p, d.ld, d.rows, d.cols, cudaMemcpyDeviceToHost, ds);
+          }
         }
       }
-    }
-    for (int q = 1; q < P; ++q) {  // join
-      cudaEvent_t join = ev();
-      cuda_check(cudaEventRecord(join, ps[q]), "record");
-      cuda_check(cudaStreamWaitEvent(cs, join, 0), "wait");
+      for (int q = 1; q < P; ++q) {  // join
+        cudaEvent_t join = ev();
+        cuda_check(cudaEventRecord(join, ps[q]), "record");
+        cuda_check(cudaStreamWaitEvent(cs, join, 0), "wait");
+      }
     }
     cuda_check(cudaGetLastError(), "kernel launch");
     cudaEvent_t t_end[3] = {nullptr, nullptr, nullptr};

@@ -397,3 +397,19 @@ def test_trmm_concurrent_halves_bitwise_serial(cuda, dt, monkeypatch):
             conc_direct = run_op("trmm", s, a, b, t, backend=Backend.cuda(flags=NO_GRAPH))
             assert oracle.bitwise_equal(ser, conc_graph), (n, s)
             assert oracle.bitwise_equal(ser, conc_direct), (n, s)
+
+
+@pytest.mark.parametrize("op", ["trsm", "trmm"])
+def test_host_streamed_time_panels(cuda, op, monkeypatch):
+    """The streamed host path in consecutive right-hand-side panels (copy-back
+    of panel t under the compute of panel t+1): bitwise the device result,
+    Left and Right, ragged last panel, alpha != 1."""
+    n, m = 1100, 150
+    monkeypatch.setenv("RECTRI_CU_E2E_PANELS", "3")
+    for side, uplo, trans, diag in [(0, 0, 0, 0), (1, 1, 1, 1), (0, 1, 0, 0), (1, 0, 0, 1)]:
+        s = oracle.spec(side, uplo, trans, diag, 0.5)
+        a = oracle.make_operand(s, op == "trsm", n, 21)
+        b = oracle.make_rhs(s, n, m, 22)
+        dev = run_op(op, s, a, b, 128)
+        host = run_op(op, s, a, b, 128, device="cpu")
+        assert oracle.bitwise_equal(dev, host), (side, uplo, trans, diag)
