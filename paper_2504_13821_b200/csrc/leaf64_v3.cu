@@ -365,13 +365,14 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
 size_t leaf3_scratch_doubles() { return leaf64v3::kScratchDoubles; }
 
 // Panel width for a leaf with nrhs right-hand sides: 32 while that still
-// gives two CTAs per SM, narrower when the leaf would leave SMs idle
+// gives every SM a CTA (8192 right-hand sides: 32-wide 70 us per 16384 vs
+// 16-wide 86, ncu launch list), narrower when the leaf would leave SMs idle
 // (RECTRI_CU_LEAF_NC = 8 / 16 / 32 forces one).  Results do not depend on it.
 int leaf3_width(long long nrhs) {
   const char* e = getenv("RECTRI_CU_LEAF_NC");
   const int forced = e ? atoi(e) : 0;
   if (forced == 8 || forced == 16 || forced == 32) return forced;
-  if (nrhs >= 32LL * 2 * 148) return 32;
+  if (nrhs >= 32LL * 148) return 32;  // at least one 32-wide CTA per SM (C3 panels: 8192)
   if (nrhs > 1024) return 16;
   return 8;
 }
