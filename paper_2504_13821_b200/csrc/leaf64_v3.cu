@@ -186,12 +186,16 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 // block (4 x NC/8 m8n8 tiles) go E per warp to CW compute warps; every
 // element's products are accumulated in the same order for every NC, so the
 // widths agree bit for bit.
-template <int NC>
+// WM = 2: a compute warp owns 2 row tiles x E column tiles (16 x 16 for
+// NC = 32, 4 compute warps): every A and B fragment feeds two DMMAs, a third
+// fewer shared-memory wavefronts per DMMA than WM = 1 (8 x 16 per warp).
+template <int NC, int WM = 1>
 __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParams<double> p,
                                                                 const double* __restrict__ P) {
   constexpr int kNC = NC;
-  constexpr int CW = NC >= 16 ? 8 : 4;           // compute warps
-  constexpr int E = 4 * (NC / 8) / CW;           // m8n8 tiles per compute warp
+  constexpr int CW = WM == 2 ? 4 : (NC >= 16 ? 8 : 4);  // compute warps
+  constexpr int E = 4 * (NC / 8) / CW / WM;              // column tiles per compute warp
+  constexpr int RW = 4 / WM;                             // warps along the rows
   extern __shared__ __align__(128) double smem3[];
   double* panel = smem3;                       // nb x 32 right-hand sides (swizzled rows)
   double* cbuf = smem3 + kLeafMax * kNC;       // TRSM: -(b_I - sum L'X) of the current row block
@@ -262,35 +266,40 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
   });
   cp_async_commit();
 
-  // warp w owns the m8n8 tiles (w & 3, 2*(w >> 2) + e), e = 0, 1.
+  // warp w owns the m8n8 tiles (mt0 + i, nt0 + e), i < WM, e < E.
   const int g = lane >> 2, t = lane & 3;
-  const int mt = warp & 3, nt0 = E * (warp >> 2);
+  const int mt0 = WM * (warp % RW), nt0 = E * (warp / RW);
   const bool computes = warp < CW;
   const uint32_t panel_u32 = smem_u32(panel), cbuf_u32 = smem_u32(cbuf);
   uint32_t b_base[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) b_base[e] = 8u * static_cast<uint32_t>(panel_idx<NC>(t, 8 * (nt0 + e) + g));
-  const uint32_t a_off = static_cast<uint32_t>((mt * 8 * 32 + lane) * 8);  // this lane's k-step-0 A fragment
+  const uint32_t a_off = static_cast<uint32_t>((mt0 * 8 * 32 + lane) * 8);  // k-step-0 A fragment, row tile mt0
   cp_async_wait<0>();
   named_sync(1, kThreads);  // panel loaded (GEMM warps only; the producer runs free)
   if (trsm && p.alpha != 1.0) {  // x = alpha * b (base_kernels.cpp:76-77)
     for_panel([&](int r, int c, const double*) { panel[panel_idx<NC>(r, c)] *= p.alpha; });
     named_sync(1, kThreads);
   }
+  // element (i, e, h) of this lane's accumulators: row 8(mt0+i)+g, column 8(nt0+e)+2t+h of the row block
+  auto crow = [&](int i) { return 8 * (mt0 + i) + g; };
+  auto ccol = [&](int e, int h) { return 8 * (nt0 + e) + 2 * t + h; };
 
-  // c[e][h] += A(block s) * Bsrc(32 rows at byte offset bsrc of a row-major
+  // c[i][e][h] += A(block s) * Bsrc(32 rows at byte offset bsrc of a row-major
   // [k][kNC] swizzled buffer)
-  double c[E][2];
+  double c[WM][E][2];
   int s = 0;
   auto block_mma = [&](uint32_t bsrc) {
     if (!computes) return;
     const int slot = s % kRing;
     mbar_wait(full0 + 8 * slot, (s / kRing) & 1);
     const uint32_t as = smem_u32(ring + slot * kBlk) + a_off;
-    double a[8];
+    double a[WM][8];
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk)
-      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[kk]) : "r"(as + kk * 32 * 8));
+    for (int i = 0; i < WM; ++i)
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[i][kk]) : "r"(as + (i * 8 + kk) * 32 * 8));
     // all 8 k-steps' B fragments first: one shared-memory latency per block
     double bv[kRB / 4][E];
 #pragma unroll
@@ -301,7 +310,9 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
 #pragma unroll
     for (int kk = 0; kk < kRB / 4; ++kk)
 #pragma unroll
-      for (int e = 0; e < E; ++e) dmma884(c[e][0], c[e][1], a[kk], bv[kk][e]);
+      for (int i = 0; i < WM; ++i)
+#pragma unroll
+        for (int e = 0; e < E; ++e) dmma884(c[i][e][0], c[i][e][1], a[i][kk], bv[kk][e]);
     // The DMMAs have consumed every fragment loaded from the slot, so those
     // loads are complete: only now release the slot to the bulk-copy proxy.
     __syncwarp();
@@ -311,47 +322,43 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
     }
     ++s;
   };
+  auto for_c = [&](auto&& f) {
+#pragma unroll
+    for (int i = 0; i < WM; ++i)
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) f(i, e, h);
+  };
 
   for (int bi = 0; bi < nblk; ++bi) {
     const int I = trsm ? bi : nblk - 1 - bi;
     const int r0 = I * kRB;
     if (trsm) {
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) c[e][h] = !computes ? 0.0 : -panel[panel_idx<NC>(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)];
+      for_c([&](int i, int e, int h) {
+        c[i][e][h] = !computes ? 0.0 : -panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))];
+      });
     } else {
-#pragma unroll
-      for (int e = 0; e < E; ++e) c[e][0] = c[e][1] = 0.0;
+      for_c([&](int i, int e, int h) { c[i][e][h] = 0.0; });
     }
     for (int J = 0; J < I; ++J) block_mma(panel_u32 + static_cast<uint32_t>(J * kRB * kNC * 8));
     if (trsm) {
       // c = -(b_I - sum L'X); X_I = (-inv(L'_II)) * c
-      if (computes)
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) cbuf[panel_idx<NC>(8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
+      if (computes) for_c([&](int i, int e, int h) { cbuf[panel_idx<NC>(crow(i), ccol(e, h))] = c[i][e][h]; });
       named_sync(1, kThreads);
-#pragma unroll
-      for (int e = 0; e < E; ++e) c[e][0] = c[e][1] = 0.0;
+      for_c([&](int i, int e, int h) { c[i][e][h] = 0.0; });
       block_mma(cbuf_u32);
       if (computes)
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) panel[panel_idx<NC>(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = c[e][h];
+        for_c([&](int i, int e, int h) { panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = c[i][e][h]; });
       named_sync(1, kThreads);  // X_I visible; cbuf free
     } else {
       // c += L'_II * b_I; every warp reads b_I before anyone overwrites it
       block_mma(panel_u32 + static_cast<uint32_t>(I * kRB * kNC * 8));
       named_sync(1, kThreads);
       if (computes)
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          panel[panel_idx<NC>(r0 + 8 * mt + g, 8 * (nt0 + e) + 2 * t + h)] = p.alpha * c[e][h];
+        for_c([&](int i, int e, int h) {
+          panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = p.alpha * c[i][e][h];
+        });
     }
   }
   named_sync(1, kThreads);
@@ -404,7 +411,9 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), kThreads + 32, smem, s>>>(p, scratch);
   };
-  if (nc == 32) go(leaf3_kernel<32>, 32, smem_bytes<32>());
+  const char* wm = getenv("RECTRI_CU_LEAF_WM");
+  if (nc == 32 && wm && atoi(wm) == 2) go(leaf3_kernel<32, 2>, 32, smem_bytes<32>());
+  else if (nc == 32) go(leaf3_kernel<32>, 32, smem_bytes<32>());
   else if (nc == 16) go(leaf3_kernel<16>, 16, smem_bytes<16>());
   else go(leaf3_kernel<8>, 8, smem_bytes<8>());
   ++launch_counter();

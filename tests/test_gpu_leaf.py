@@ -120,8 +120,10 @@ def test_leaf_v3_panel_widths_bitwise(cuda, monkeypatch, dt, op, side, uplo, tra
         a, b = _inputs(op, s, n, m, rng)
         a, b = F(a.astype(dt)), F(b.astype(dt))
         outs = []
-        for nc in ("32", "16", "8"):
+        for nc, wm in (("32", "1"), ("16", "1"), ("8", "1"), ("32", "2")):
             monkeypatch.setenv("RECTRI_CU_LEAF_NC", nc)
+            monkeypatch.setenv("RECTRI_CU_LEAF_WM", wm)
             outs.append(_base(op, s, a, b, 3, monkeypatch))
         check_against_oracle(op, s, a, b, outs[0])
-        assert oracle.bitwise_equal(outs[0], outs[1]) and oracle.bitwise_equal(outs[0], outs[2]), (n, m)
+        for k, o in enumerate(outs[1:], 1):
+            assert oracle.bitwise_equal(outs[0], o), (n, m, k)
