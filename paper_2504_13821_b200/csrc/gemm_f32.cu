@@ -369,6 +369,44 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
   cp_async_wait<0>();
 
   const bool beta_zero = p.beta == 0.f;
+  // Full-height tile with a 16-byte aligned C: each column's 8 values are two
+  // float4 runs (rows 4ty.., BM/2 + 4ty..), and the reads of 4 columns are
+  // issued before their writes -- two dependent round trips per thread
+  // instead of eight (short-K updates stall on exactly these reads).
+  const bool vec = m0 + BM <= p.M && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && p.ldc % 4 == 0;
+  if (vec) {
+#pragma unroll
+    for (int jb = 0; jb < 8; jb += 4) {
+      float4 cv[4][2];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const i64 n = n0 + FFrag<BN, false>::outer(tx, jb + jj);
+        const float* cp = p.C + m0 + 4 * ty + n * p.ldc;
+        const bool rd = !beta_zero && n < p.N;
+        cv[jj][0] = rd ? *reinterpret_cast<const float4*>(cp) : make_float4(0.f, 0.f, 0.f, 0.f);
+        cv[jj][1] = rd ? *reinterpret_cast<const float4*>(cp + BM / 2) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = jb + jj;
+        const i64 n = n0 + FFrag<BN, false>::outer(tx, j);
+        if (n >= p.N) continue;
+        float a[8];
+#pragma unroll
+        for (int ip = 0; ip < 4; ++ip)
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(a[2 * ip]), "=f"(a[2 * ip + 1]) : "l"(acc2[ip][j]));
+        const float co[8] = {cv[jj][0].x, cv[jj][0].y, cv[jj][0].z, cv[jj][0].w,
+                             cv[jj][1].x, cv[jj][1].y, cv[jj][1].z, cv[jj][1].w};
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = beta_zero ? p.alpha * a[i] : fmaf(p.alpha, a[i], p.beta * co[i]);
+        float* cp = p.C + m0 + 4 * ty + n * p.ldc;
+        *reinterpret_cast<float4*>(cp) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4*>(cp + BM / 2) = make_float4(o[4], o[5], o[6], o[7]);
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const i64 n = n0 + FFrag<BN, false>::outer(tx, j);

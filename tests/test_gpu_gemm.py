@@ -166,3 +166,24 @@ def test_sgemm_v2_bitwise_equals_v1(cuda, ta, tb, monkeypatch):
                 outs.append(to_np(C))
             assert oracle.bitwise_equal(outs[0], outs[1]), (M, N, K, off, alpha, beta)
             assert oracle.bitwise_equal(outs[0], outs[2]), (M, N, K, off, alpha, beta, "bk32")
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_sgemm_v2_vector_epilogue_bitwise(cuda, ta, tb, monkeypatch):
+    """Full-height tiles with a 16-byte aligned C take the float4 epilogue
+    (reads of four columns before their writes): bitwise v1, ragged N, beta
+    0 and != 0; a ragged M (the scalar epilogue) alongside."""
+    rng = np.random.default_rng(13)
+    for (M, N, K), beta in itertools.product(((256, 200, 300), (128, 129, 64), (250, 130, 40)), (1.0, 0.0, -0.5)):
+        a = F(rng.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32))
+        b = F(rng.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32))
+        ld = (M + 3) // 4 * 4 + 4
+        c0 = F(rng.uniform(-1, 1, (ld, N)).astype(np.float32))
+        A, B = to_dev(a), to_dev(b)
+        outs = []
+        for ver in ("1", "2"):
+            monkeypatch.setenv("RECTRI_CU_SGEMM", ver)
+            C = to_dev(c0)
+            gemm(0.75, Trans(ta), A.cview(), Trans(tb), B.cview(), beta, C.view().subview(0, 0, M, N))
+            outs.append(to_np(C))
+        assert oracle.bitwise_equal(outs[0], outs[1]), (M, N, K, beta)
