@@ -24,12 +24,13 @@ def _san(tool, args, env_extra=None):
 
 @pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
 @pytest.mark.parametrize("args", [["leaf", "100", "70"], ["trmmleaf", "100", "70"], ["gemm", "130", "70", "50"], ["gemm", "200", "130", "1100"],
-                                  ["trsm", "300", "40", "64"]])
+                                  ["trsm", "300", "40", "64"], ["sgemm", "130", "70", "50"], ["sgemm", "256", "200", "300"],
+                                  ["leaf32", "100", "70"], ["strsm", "300", "40", "64"], ["trmm", "520", "40", "32"]])
 def test_kernels_clean(cuda, tool, args):
     # racecheck does not model mbarrier-ordered cp.async.bulk ring refills
     # (the default fp64 leaf, leaf64_v3.cu, reports its ring as a hazard); it
     # checks the barrier-synchronised v2 leaf, the other tools the default.
-    env = {"RECTRI_CU_LEAF": "2"} if tool == "racecheck" and args[0] != "gemm" else None
+    env = {"RECTRI_CU_LEAF": "2"} if tool == "racecheck" and "gemm" not in args[0] else None
     r = _san(tool, args, env)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-3000:]
