@@ -317,12 +317,21 @@ struct KDesc {
 // out) nodes run serially.
 template <typename T>
 struct ConcCtx {
-  std::vector<cudaStream_t>* streams = nullptr;
-  std::vector<cudaEvent_t>* events = nullptr;
-  size_t next_stream = 0, next_event = 0;
+  std::vector<cudaStream_t>* streams = nullptr;  // per device: one pool for captures, one for direct calls
+  std::vector<cudaEvent_t> events;               // this call's fork/join events (never shared across calls)
+  size_t next_stream = 0;
   T* scratch = nullptr;
   i64 cap = 0, used = 0;
   static constexpr i64 kMaxElems = i64(1) << 21;  // per node: mid x rhs
+  cudaEvent_t event() {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    events.push_back(e);
+    return e;
+  }
+  ~ConcCtx() {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+  }
 };
 
 template <typename T>
@@ -405,16 +414,15 @@ class Recursion {
   bool conc_node(const Schema& sc, i64 mid, i64 rhs, DView<T> dst) {
     if (!conc || dry_ || kernels || op_ != kTrmm || mid * rhs > ConcCtx<T>::kMaxElems) return false;
     if (sc.first_a22 != sc.write_b2) return false;  // first half must be the GEMM's destination
-    return conc->next_stream < conc->streams->size() && conc->next_event + 2 <= conc->events->size() &&
-           conc->used + dst.rows * dst.cols <= conc->cap;
+    return conc->next_stream < conc->streams->size() && conc->used + dst.rows * dst.cols <= conc->cap;
   }
 
   void run_concurrent(const Spec& spec, const Schema& sc, DView<const T> a11, DView<const T> a22,
                       DView<const T> off, DView<T> b1, DView<T> b2, DView<T> dst, DView<const T> src,
                       T coeff, i64 mid, i64 row0) {
     cudaStream_t s2 = (*conc->streams)[conc->next_stream++];
-    cudaEvent_t fork = (*conc->events)[conc->next_event++];
-    cudaEvent_t join = (*conc->events)[conc->next_event++];
+    cudaEvent_t fork = conc->event();
+    cudaEvent_t join = conc->event();
     const DView<T> S{conc->scratch + conc->used, dst.rows, dst.rows, dst.cols};
     conc->used += dst.rows * dst.cols;
     cuda_check(cudaEventRecord(fork, s_), "record fork");
@@ -507,8 +515,8 @@ struct DeviceRes {
   cudaStream_t capture = nullptr;
   cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr};
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the staged path
-  std::vector<cudaStream_t> conc_streams;     // concurrent TRMM nodes (ConcCtx)
-  std::vector<cudaEvent_t> conc_events;
+  std::vector<cudaStream_t> conc_streams;      // concurrent TRMM nodes (ConcCtx), graph captures (under g_mu)
+  std::vector<cudaStream_t> conc_streams_dir;  // the same for direct-launch calls
   static constexpr int kSlots = 3;            // 0: A, 1..2: B panels
   void* stage[kSlots] = {nullptr, nullptr, nullptr};
   size_t stage_bytes[kSlots] = {0, 0, 0};
@@ -526,8 +534,8 @@ DeviceRes& device_res(int dev) {
     for (auto& a : r.aux) cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
     r.conc_streams.resize(16);
     for (auto& a : r.conc_streams) cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
-    r.conc_events.resize(64);
-    for (auto& e : r.conc_events) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    r.conc_streams_dir.resize(16);
+    for (auto& a : r.conc_streams_dir) cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
   }
   return r;
 }
@@ -707,8 +715,7 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
         resp = &device_res(dev);
       }
       cuda_check(cudaMalloc(&g->conc_scratch, static_cast<size_t>(need) * sizeof(T)), "trmm scratch alloc");
-      conc.streams = &resp->conc_streams;
-      conc.events = &resp->conc_events;
+      conc.streams = capture ? &resp->conc_streams : &resp->conc_streams_dir;
       conc.scratch = static_cast<T*>(g->conc_scratch);
       conc.cap = need;
     }
