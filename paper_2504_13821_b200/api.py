@@ -331,7 +331,7 @@ class Backend:
         if dev < 0 and tensor_device is not None and tensor_device.type == "cuda":
             dev = tensor_device.index if tensor_device.index is not None else torch.cuda.current_device()
         if stream is None:
-            handle = torch.cuda.current_stream(dev if dev >= 0 else None).cuda_stream if torch.cuda.is_available() else 0
+            handle = _current_stream_handle(dev)
         elif isinstance(stream, int):
             handle = stream
         else:
@@ -400,6 +400,19 @@ class RecEvent(enum.IntEnum):
 EventSink = Callable[[RecEvent, int, int], None]
 
 
+def _current_stream_handle(dev: int) -> int:
+    """torch's current stream on `dev` as a raw handle (the raw accessor skips
+    building a torch.cuda.Stream object: ~0.3 us instead of ~3 us per call)."""
+    if not torch.cuda.is_available():
+        return 0
+    d = dev if dev >= 0 else torch.cuda.current_device()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    return raw(d) if raw is not None else torch.cuda.current_stream(d).cuda_stream
+
+
+_NULL_SINK = None
+
+
 def _spec_c(spec: TriangularSpec) -> _lib.Spec:
     return _lib.Spec(int(spec.side), int(spec.uplo), int(spec.trans), int(spec.diag), float(spec.alpha))
 
@@ -422,8 +435,11 @@ def _suffix(a: MatrixView, b: MatrixView) -> str:
 
 
 def _sink_c(sink: Optional[EventSink]):
+    global _NULL_SINK
     if sink is None:
-        return _lib.EVENT_FN(), None
+        if _NULL_SINK is None:
+            _NULL_SINK = _lib.EVENT_FN()
+        return _NULL_SINK, None
     errors = []
 
     def tramp(_user, ev, n, m):
