@@ -517,6 +517,7 @@ struct DeviceRes {
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the staged path
   std::vector<cudaStream_t> conc_streams;      // concurrent TRMM nodes (ConcCtx), graph captures (under g_mu)
   std::vector<cudaStream_t> conc_streams_dir;  // the same for direct-launch calls
+  cudaStream_t scan_cap = nullptr, scan_dir = nullptr;  // zero-pivot scan beside the recursion
   static constexpr int kSlots = 3;            // 0: A, 1..2: B panels
   void* stage[kSlots] = {nullptr, nullptr, nullptr};
   size_t stage_bytes[kSlots] = {0, 0, 0};
@@ -534,6 +535,8 @@ DeviceRes& device_res(int dev) {
     for (auto& a : r.aux) cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
     r.conc_streams.resize(16);
     for (auto& a : r.conc_streams) cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&r.scan_cap, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&r.scan_dir, cudaStreamNonBlocking), "stream");
     r.conc_streams_dir.resize(16);
     for (auto& a : r.conc_streams_dir) cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
   }
@@ -758,10 +761,30 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
     if (conc.scratch) r.conc = &conc;
     return r;
   };
-  if (scan) {
+  // The zero-pivot scan only reads A and its flags are read on the host after
+  // the call: it runs on a side stream beside the recursion (joined at the
+  // end) instead of ahead of it -- one kernel plus one D2H off every TRSM
+  // NonUnit call's critical path.
+  cudaEvent_t scan_ev[2] = {nullptr, nullptr};
+  if (scan && g_prof.on) {
     ProfScope prof(3, 0.0, s);
     K<T>::scan(A.p, A.ld, A.rows, g->d_flags, s);
     cudaMemcpyAsync(g->h_flags, g->d_flags, static_cast<size_t>(A.rows), cudaMemcpyDeviceToHost, s);
+  } else if (scan) {
+    DeviceRes* rp;
+    if (capture) {  // the capture path already holds g_mu
+      rp = &device_res(dev);
+    } else {
+      std::lock_guard<std::mutex> lock(g_mu);
+      rp = &device_res(dev);
+    }
+    cudaStream_t ss = capture ? rp->scan_cap : rp->scan_dir;
+    for (auto& e : scan_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(scan_ev[0], s), "record");
+    cuda_check(cudaStreamWaitEvent(ss, scan_ev[0], 0), "wait");
+    K<T>::scan(A.p, A.ld, A.rows, g->d_flags, ss);
+    cudaMemcpyAsync(g->h_flags, g->d_flags, static_cast<size_t>(A.rows), cudaMemcpyDeviceToHost, ss);
+    cuda_check(cudaEventRecord(scan_ev[1], ss), "record");
   }
   const bool left = spec.side == RECTRI_CU_LEFT;
   const i64 rhs = left ? B.cols : B.rows;
@@ -811,7 +834,10 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
     }
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
   }
+  if (scan_ev[1]) cuda_check(cudaStreamWaitEvent(s, scan_ev[1], 0), "wait scan");
   cudaError_t le = cudaGetLastError();
+  for (cudaEvent_t e : scan_ev)
+    if (e) cudaEventDestroy(e);
   if (capture) {
     cudaGraph_t graph = nullptr;
     cudaError_t ee = cudaStreamEndCapture(s, &graph);
