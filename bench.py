@@ -463,6 +463,7 @@ def main():
                "d2h_bytes_per_step": n * me * 8 * world,
                "rhs_per_gpu": me,
                "ms_per_step": wall / args.steps * 1e3,
+               "step_ms": [round(w * 1e3, 2) for w in walls],
                "path": "rectri_cu_rec_trsm_f64 with pinned host views: A blocks and B row chunks copied in "
                        "first-use order, each kernel gated on its own inputs, chunks copied back after their "
                        "last writer (driver.cu run_host_streamed); wall clock"}

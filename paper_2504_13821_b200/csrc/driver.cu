@@ -1171,15 +1171,16 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
       cuda_check(cudaMemcpyAsync(h_flags, d_flags, static_cast<size_t>(n), cudaMemcpyDeviceToHost, cs), "flags");
     }
     // Right-hand sides in TP consecutive time panels (RECTRI_CU_E2E_PANELS;
-    // default 2 from 16384 right-hand sides): panel t's chunks are copied back
+    // default: ~8192-wide panels): panel t's chunks are copied back
     // while panel t+1 computes, so only the last panel's last rows are left
     // for the tail (C3: compute done 132.3 -> 130.2 ms, tail 6.6 -> 3.3 ms,
     // e2e 139.3 -> 134.3 ms; 4 panels: tail 1.4 ms but the narrower GEMMs
-    // finish at 137 ms).  Within a panel the right-hand sides are split over P
+    // finish at 137 ms.  C5 slice n = 8192, 65536 columns: 1 / 2 / 4 / 8
+    // panels 178 / 155 / 144 / 143 ms).  Within a panel the right-hand sides are split over P
     // streams as in the device path.  Arithmetic is per right-hand side, so
     // the result is bitwise the single-panel one.
     const i64 rhs = left ? bcols : brows;
-    int TP = rhs >= 16384 ? 2 : 1;
+    int TP = static_cast<int>(std::max<i64>(1, std::min<i64>(16, rhs / 8192)));
     if (const char* te = getenv("RECTRI_CU_E2E_PANELS")) TP = std::max(1, atoi(te));
     const i64 tw = (rhs + TP - 1) / TP;
     auto window = [&](DView<T> v, i64 r0, i64 r1) {
