@@ -322,7 +322,8 @@ struct ConcCtx {
   size_t next_stream = 0;
   T* scratch = nullptr;
   i64 cap = 0, used = 0;
-  static constexpr i64 kMaxElems = i64(1) << 21;  // per node: mid x rhs
+  static constexpr i64 kMaxElems = i64(1) << 21;  // per node: mid x rhs (default)
+  i64 max_elems = kMaxElems;
   cudaEvent_t event() {
     cudaEvent_t e;
     cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -355,11 +356,11 @@ class Recursion {
   ConcCtx<T>* conc = nullptr;
 
   // Scratch elements the concurrent TRMM nodes of run(n, rhs) use.
-  static i64 conc_need(OpK op, i64 threshold, i64 n, i64 rhs) {
+  static i64 conc_need(OpK op, i64 threshold, i64 n, i64 rhs, i64 max_elems) {
     if (op != kTrmm || n <= threshold) return 0;
     const i64 mid = n / 2, big = n - mid;
-    const i64 own = mid * rhs <= ConcCtx<T>::kMaxElems ? big * rhs : 0;
-    return own + conc_need(op, threshold, mid, rhs) + conc_need(op, threshold, big, rhs);
+    const i64 own = mid * rhs <= max_elems ? big * rhs : 0;
+    return own + conc_need(op, threshold, mid, rhs, max_elems) + conc_need(op, threshold, big, rhs, max_elems);
   }
 
   // recursion.cpp:85-148
@@ -412,7 +413,7 @@ class Recursion {
 
  private:
   bool conc_node(const Schema& sc, i64 mid, i64 rhs, DView<T> dst) {
-    if (!conc || dry_ || kernels || op_ != kTrmm || mid * rhs > ConcCtx<T>::kMaxElems) return false;
+    if (!conc || dry_ || kernels || op_ != kTrmm || mid * rhs > conc->max_elems) return false;
     if (sc.first_a22 != sc.write_b2) return false;  // first half must be the GEMM's destination
     return conc->next_stream < conc->streams->size() && conc->used + dst.rows * dst.cols <= conc->cap;
   }
@@ -703,12 +704,15 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
   const i64 rhs_ = left_ ? B.cols : B.rows;
   const int P_ = g_prof.on ? 1 : panel_streams(rhs_);
   // Only where the GPU is not already full: n <= 4096 (fp64) / 8192 (fp32).
-  const i64 conc_max_n = sizeof(T) == 8 ? 4096 : 8192;
+  i64 conc_max_n = sizeof(T) == 8 ? 4096 : 8192;
+  if (const char* e = getenv("RECTRI_CU_TRMM_CONC_MAXN")) conc_max_n = atoll(e);
   if (op == kTrmm && nleaves > 0 && !g_prof.on && conc_enabled() && A.rows <= conc_max_n &&
       !(std::is_same<T, float>::value && tf32x3_enabled())) {
     const i64 w = P_ <= 1 ? rhs_ : ((rhs_ + P_ - 1) / P_ + 63) / 64 * 64;
     i64 need = 0;
-    for (i64 r0 = 0; r0 < rhs_; r0 += w) need += Recursion<T>::conc_need(op, threshold, A.rows, std::min(w, rhs_ - r0));
+    if (const char* e = getenv("RECTRI_CU_TRMM_CONC_ELEMS")) conc.max_elems = atoll(e);
+    for (i64 r0 = 0; r0 < rhs_; r0 += w)
+      need += Recursion<T>::conc_need(op, threshold, A.rows, std::min(w, rhs_ - r0), conc.max_elems);
     if (need > 0 && need * static_cast<i64>(sizeof(T)) <= (i64(512) << 20)) {
       DeviceRes* resp;
       if (capture) {  // the capture path already holds g_mu
