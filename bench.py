@@ -464,6 +464,7 @@ def main():
                "rhs_per_gpu": me,
                "ms_per_step": wall / args.steps * 1e3,
                "step_ms": [round(w * 1e3, 2) for w in walls],
+               "median_step_ms": round(sorted(walls)[len(walls) // 2] * 1e3, 2),
                "path": "rectri_cu_rec_trsm_f64 with pinned host views: A blocks and B row chunks copied in "
                        "first-use order, each kernel gated on its own inputs, chunks copied back after their "
                        "last writer (driver.cu run_host_streamed); wall clock"}
