@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdarg>
@@ -1167,6 +1168,7 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
     cuda_check(cudaEventCreate(&start), "event");  // timed (RECTRI_CU_E2E_TRACE)
     evs.push_back(start);
     cuda_check(cudaEventRecord(start, cs), "record");  // staging buffers free (stream order)
+    const auto host_t0 = std::chrono::steady_clock::now();
     cuda_check(cudaStreamWaitEvent(hs, start, 0), "wait");
     if (scan && a_dev) {
       cuda_check(cudaMalloc(&d_flags, static_cast<size_t>(n)), "flags alloc");
@@ -1325,10 +1327,13 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
       cudaEventRecord(t_end[1], cs);
       cudaEventRecord(t_end[2], ds);
     }
+    const double host_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
     cuda_check(cudaStreamSynchronize(ds), "synchronize");
     cuda_check(cudaStreamSynchronize(cs), "synchronize");
     cuda_check(cudaStreamSynchronize(hs), "synchronize");
     if (trace) {
+      fprintf(stderr, "e2e trace: host enqueue %.2f ms\n", host_ms);
       float t[3] = {0, 0, 0};
       for (int q = 0; q < 3; ++q) cudaEventElapsedTime(&t[q], start, t_end[q]);
       fprintf(stderr, "e2e trace: h2d done %.2f ms, compute done %.2f ms, d2h done %.2f ms, %zu units, %d chunks\n",
