@@ -285,9 +285,12 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
   auto crow = [&](int i) { return 8 * (mt0 + i) + g; };
   auto ccol = [&](int e, int h) { return 8 * (nt0 + e) + 2 * t + h; };
 
-  // c[i][e][h] += A(block s) * Bsrc(32 rows at byte offset bsrc of a row-major
-  // [k][kNC] swizzled buffer)
-  double c[WM][E][2];
+  // c[q][i][e][h] += A(block s) * Bsrc(32 rows at byte offset bsrc of a
+  // row-major [k][kNC] swizzled buffer), k-steps alternating between the two
+  // partial sums q = kk & 1 (two independent DMMA chains per tile: half the
+  // dependency latency of a leaf with few right-hand sides); the partial
+  // sums are added once per row block.  Same order for every NC and WM.
+  double c[2][WM][E][2];
   int s = 0;
   auto block_mma = [&](uint32_t bsrc) {
     if (!computes) return;
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
 #pragma unroll
       for (int i = 0; i < WM; ++i)
 #pragma unroll
-        for (int e = 0; e < E; ++e) dmma884(c[i][e][0], c[i][e][1], a[i][kk], bv[kk][e]);
+        for (int e = 0; e < E; ++e) dmma884(c[kk & 1][i][e][0], c[kk & 1][i][e][1], a[i][kk], bv[kk][e]);
     // The DMMAs have consumed every fragment loaded from the slot, so those
     // loads are complete: only now release the slot to the bulk-copy proxy.
     __syncwarp();
@@ -336,20 +339,24 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
     const int r0 = I * kRB;
     if (trsm) {
       for_c([&](int i, int e, int h) {
-        c[i][e][h] = !computes ? 0.0 : -panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))];
+        c[0][i][e][h] = !computes ? 0.0 : -panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))];
+        c[1][i][e][h] = 0.0;
       });
     } else {
-      for_c([&](int i, int e, int h) { c[i][e][h] = 0.0; });
+      for_c([&](int i, int e, int h) { c[0][i][e][h] = c[1][i][e][h] = 0.0; });
     }
     for (int J = 0; J < I; ++J) block_mma(panel_u32 + static_cast<uint32_t>(J * kRB * kNC * 8));
     if (trsm) {
       // c = -(b_I - sum L'X); X_I = (-inv(L'_II)) * c
-      if (computes) for_c([&](int i, int e, int h) { cbuf[panel_idx<NC>(crow(i), ccol(e, h))] = c[i][e][h]; });
+      if (computes)
+        for_c([&](int i, int e, int h) { cbuf[panel_idx<NC>(crow(i), ccol(e, h))] = c[0][i][e][h] + c[1][i][e][h]; });
       named_sync(1, kThreads);
-      for_c([&](int i, int e, int h) { c[i][e][h] = 0.0; });
+      for_c([&](int i, int e, int h) { c[0][i][e][h] = c[1][i][e][h] = 0.0; });
       block_mma(cbuf_u32);
       if (computes)
-        for_c([&](int i, int e, int h) { panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = c[i][e][h]; });
+        for_c([&](int i, int e, int h) {
+          panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = c[0][i][e][h] + c[1][i][e][h];
+        });
       named_sync(1, kThreads);  // X_I visible; cbuf free
     } else {
       // c += L'_II * b_I; every warp reads b_I before anyone overwrites it
@@ -357,7 +364,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
       named_sync(1, kThreads);
       if (computes)
         for_c([&](int i, int e, int h) {
-          panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = p.alpha * c[i][e][h];
+          panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = p.alpha * (c[0][i][e][h] + c[1][i][e][h]);
         });
     }
   }
