@@ -298,6 +298,8 @@ def main():
         barrier(world)
         launches0 = rc.launch_count()
         evs = []
+        gc.collect()
+        gc.disable()  # no cycle collection between a step's events (see the e2e loop)
         with ClockSampler(local) as clk:
             for _ in range(args.steps):
                 Bbuf.data.copy_(B0buf.data)
@@ -309,6 +311,7 @@ def main():
                 evs.append((e0, e1))
             rc.sync(stream)
             torch.cuda.synchronize()
+        gc.enable()
         launches = rc.launch_count() - launches0
         barrier(world)
         local_ms = sum(a.elapsed_time(b) for a, b in evs)
