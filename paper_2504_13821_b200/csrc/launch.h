@@ -71,7 +71,7 @@ void launch_leaf3_pack_all(const LeafParams<double>& base, const long long* d_r0
 size_t leaf3_scratch_doubles();
 // Packs one leaf's triangle (p.A, p.n, variant flags) into dst.
 void launch_leaf3_pack(const LeafParams<double>& p, double* dst, cudaStream_t s);
-int leaf3_width(long long nrhs);  // fp64 leaf v3 panel width (8 / 16 / 32)
+int leaf3_width(long long nrhs, bool trsm);  // fp64 leaf v3 panel width (8 / 16 / 32)
 int leaf_version();  // RECTRI_CU_LEAF (fp64: 1 = leaf.cu, 2 = leaf64.cu, 3 = leaf64_v3.cu)
 // Allocates the v2 fp64 leaf's per-stream scratch (call before capturing on s).
 void leaf_scratch_reserve(cudaStream_t s);

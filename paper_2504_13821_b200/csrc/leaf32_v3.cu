@@ -355,7 +355,7 @@ void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), 4 * width + 32, smem, s>>>(p, scratch);
   };
-  const int nc = leaf3_width(p.nrhs);
+  const int nc = leaf3_width(p.nrhs, p.trsm != 0);
   if (nc == 32) go(leaf32_kernel<32>, 32, smem_bytes<32>());
   else if (nc == 16) go(leaf32_kernel<16>, 16, smem_bytes<16>());
   else go(leaf32_kernel<8>, 8, smem_bytes<8>());

@@ -382,12 +382,16 @@ size_t leaf3_scratch_doubles() { return leaf64v3::kScratchDoubles; }
 // gives every SM a CTA (8192 right-hand sides: 32-wide 70 us per 16384 vs
 // 16-wide 86, ncu launch list), narrower when the leaf would leave SMs idle
 // (RECTRI_CU_LEAF_NC = 8 / 16 / 32 forces one).  Results do not depend on it.
-int leaf3_width(long long nrhs) {
+int leaf3_width(long long nrhs, bool trsm) {
   const char* e = getenv("RECTRI_CU_LEAF_NC");
   const int forced = e ? atoi(e) : 0;
   if (forced == 8 || forced == 16 || forced == 32) return forced;
   if (nrhs >= 32LL * 148) return 32;  // at least one 32-wide CTA per SM (C3 panels: 8192)
-  if (nrhs > 1024) return 16;
+  // TRSM leaves sit on the critical path (X1 -> GEMM -> X2): narrowest panels
+  // up to 1024 right-hand sides; TRMM leaves overlap the other half's GEMM
+  // (concurrent halves), where 16-wide ones do better (n = m = 1024: 72.5 vs
+  // 84.8 us; TRSM 107.9 vs 117.9 the other way round).
+  if (nrhs > (trsm ? 1024 : 512)) return 16;
   return 8;
 }
 
@@ -413,7 +417,7 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
     pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, scratch);
     ++launch_counter();
   }
-  const int nc = leaf3_width(p.nrhs);
+  const int nc = leaf3_width(p.nrhs, p.trsm != 0);
   auto go = [&](auto kern, int width, int smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), kThreads + 32, smem, s>>>(p, scratch);
