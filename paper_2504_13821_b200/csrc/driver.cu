@@ -711,6 +711,11 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
       !(std::is_same<T, float>::value && tf32x3_enabled())) {
     const i64 w = P_ <= 1 ? rhs_ : ((rhs_ + P_ - 1) / P_ + 63) / 64 * 64;
     i64 need = 0;
+    // At the largest concurrent sizes (fp64 4096, fp32 8192) only the deepest
+    // nodes (their full-size halves already fill the GPU): fp64 TRMM n = 4096
+    // 2239 -> 2203 us, fp32 n = 8192 11.71 -> 11.57 ms; smaller calls: every
+    // node (fp32 n = 4096 with the cut: 1859 -> 1992 us).
+    if (A.rows >= conc_max_n) conc.max_elems = i64(1) << 19;
     if (const char* e = getenv("RECTRI_CU_TRMM_CONC_ELEMS")) conc.max_elems = atoll(e);
     for (i64 r0 = 0; r0 < rhs_; r0 += w)
       need += Recursion<T>::conc_need(op, threshold, A.rows, std::min(w, rhs_ - r0), conc.max_elems);
