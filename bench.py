@@ -103,30 +103,84 @@ def env_int(k, d):
     return int(os.environ.get(k, d))
 
 
+def spawn_ranks(args) -> int | None:
+    """`--gpus N` (N > 1) outside torchrun: re-launch this script as N ranks
+    (one process per GPU) under torch.distributed.run on 127.0.0.1 and return
+    the exit code; None when already a rank (or N == 1)."""
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1:
+        return None
+    import socket
+    import subprocess
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    log("bench: spawning " + " ".join(cmd))
+    return subprocess.call(cmd, env=dict(os.environ))
+
+
 def setup_dist(args):
+    """One process per GPU.  Under torchrun (WORLD_SIZE set) the process group
+    is created even at world size 1, so the NCCL init, the in-step broadcast
+    of A and the max-over-ranks all-reduce run on every launch of this kind;
+    NCCL's INIT lines go to stderr as evidence of the communicator size."""
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if "WORLD_SIZE" in os.environ:
+        if args.dry_gloo:
+            dist.init_process_group("gloo")
+        else:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        log(f"bench: rank {dist.get_rank()} of {dist.get_world_size()} ({dist.get_backend()}), local rank {local}")
+        if args.gpus != world:
+            log(f"bench: note --gpus {args.gpus} but WORLD_SIZE {world}; the launcher's world size is used")
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
 
 
 def allmax(x: float, world: int) -> float:
-    if world == 1:
+    if not dist.is_initialized():
         return x
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
 def barrier(world):
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
     torch.cuda.synchronize()
+
+
+def bind_to_gpu_numa_node(index: int):
+    """Pins this process to the CPUs NVML reports as local to the GPU (its
+    NUMA node), so pinned host buffers are first-touched on the GPU's node.
+    Returns the previous affinity (restored for the CPU baseline)."""
+    prev = os.sched_getaffinity(0)
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = (os.cpu_count() + 63) // 64
+        mask = pynvml.nvmlDeviceGetCpuAffinity(h, words)
+        cpus = {64 * w + b for w, m in enumerate(mask) for b in range(64) if (int(m) >> b) & 1}
+        cpus &= prev
+        if cpus and cpus != prev:
+            os.sched_setaffinity(0, cpus)
+            log(f"bench: bound to the {len(cpus)} CPUs local to GPU {index}")
+    except Exception as e:  # pragma: no cover - NVML absent
+        log(f"bench: no NUMA binding ({e})")
+    return prev
 
 
 # ------------------------------------------------------------ reference arm
@@ -147,9 +201,14 @@ def run_reference(args, world, rank):
     if ref.available():
         kind = "reference"
 
+        b0 = b.copy(order="F")
+
         def step():
+            np.copyto(b, b0)  # restore B (outside the timer: see the loop below)
+            t0 = time.perf_counter()
             st, _, _, _ = ref.rec(args.op_headline, spec, a, b, args.ref_threshold, width=-1)
             assert st == 0, ref.last_error()
+            return time.perf_counter() - t0
     else:  # the C restatement (single thread, naive) on a tiny slice
         kind = "port"
         m_s = 8
@@ -157,14 +216,12 @@ def run_reference(args, world, rank):
         cores = 1
 
         def step():
+            t0 = time.perf_counter()
             (oracle.oracle_trsm if args.op_headline == "trsm" else oracle.oracle_trmm)(spec, a, b)
+            return time.perf_counter() - t0
     for _ in range(args.warmup):
         step()
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        step()
-        times.append(time.perf_counter() - t0)
+    times = [step() for _ in range(args.steps)]
     t = statistics.median(times)
     value = n * n * m_s / t / 1e9
     sample = (f"{args.op_headline} left-{'lower' if args.op_headline == 'trsm' else 'upper'}-n-nonunit fp64 "
@@ -211,6 +268,103 @@ def workload_config(args, world):
     }
 
 
+def run_dry(args, world, rank):
+    """`--dry-gloo`: the multi-rank plumbing of the bench without a GPU --
+    the spawn, the rendezvous, the in-step broadcast of A from rank 0 and the
+    max-over-ranks of the step time, on gloo.  Prints a JSON line with no
+    value (nothing is computed)."""
+    n = 64
+    A = torch.arange(n * n, dtype=torch.float64).reshape(n, n) if rank == 0 else torch.zeros(n, n, dtype=torch.float64)
+    steps = []
+    for _ in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if dist.is_initialized():
+            dist.broadcast(A, src=0)
+        steps.append(time.perf_counter() - t0)
+    ok = bool(torch.equal(A, torch.arange(n * n, dtype=torch.float64).reshape(n, n)))
+    oks = allmax(0.0 if ok else 1.0, world)
+    ms = allmax(sum(steps[args.warmup:]) * 1e3, world)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms / max(args.steps, 1), "dry_run": True,
+                          "backend": dist.get_backend() if dist.is_initialized() else None,
+                          "broadcast_ok": oks == 0.0, "config": workload_config(args, world)}), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def run_c5(args, world, rank, local, rc, stream):
+    """North-star strong-scaling line (BASELINE configs[4], "C5"): TRSM
+    L/L/N/NU fp64, n = 8192, m = 524288 right-hand sides in TOTAL, column-
+    sharded (m / N per GPU, values keyed by the global column), A broadcast
+    from rank 0 inside every timed step; time = max over ranks of the summed
+    per-step CUDA events.  B is regenerated between steps outside the events."""
+    from paper_2504_13821_b200 import ASYNC, Backend, Diag, MatrixBuffer, Side, Threshold, Trans, TriangularSpec, Uplo
+
+    n, m_total = 8192, 524288
+    m = m_total // world
+    dev = torch.device("cuda", local)
+    A = MatrixBuffer(n, n, torch.float64, dev)
+    if rank == 0:
+        rc.fill_uniform(A.view(), 0, n, seed=11)
+        rc.make_dominant(A.view(), Uplo.Lower)
+    B = MatrixBuffer(n, m, torch.float64, dev)
+    spec = TriangularSpec(Side.Left, Uplo.Lower, Trans.NoTrans, Diag.NonUnit, 1.0)
+    be = Backend.cuda(device=local, stream=stream, flags=ASYNC)
+    torch.cuda.synchronize()
+
+    def step():
+        if dist.is_initialized():
+            dist.broadcast(A.data, src=0)
+        rc.rec_trsm(spec, A.cview(), B.view(), Threshold(args.threshold), be)
+
+    for _ in range(1):  # graph capture
+        rc.fill_uniform(B.view(), col0=rank * m, global_rows=n, seed=12)
+        step()
+    rc.sync(stream)
+    barrier(world)
+    evs = []
+    gc.collect()
+    gc.disable()
+    with ClockSampler(local) as clk:
+        for _ in range(args.c5_steps):
+            rc.fill_uniform(B.view(), col0=rank * m, global_rows=n, seed=12, backend=be)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            evs.append((e0, e1))
+        rc.sync(stream)
+        torch.cuda.synchronize()
+    gc.enable()
+    barrier(world)
+    ms = allmax(sum(a.elapsed_time(b) for a, b in evs), world) / args.c5_steps
+    # residual on 8 sampled columns of this rank's shard (pristine values regenerated by global column)
+    cols = [k * (m // 8) for k in range(8)]
+    Bs = MatrixBuffer(n, 8, torch.float64, dev)
+    for j, c in enumerate(cols):
+        rc.fill_uniform(Bs.view().subview(0, j, n, 1), col0=rank * m + c, global_rows=n, seed=12)
+    torch.cuda.synchronize()
+    X = B.data[cols].t()
+    L = torch.tril(A.data.t())
+    Bsd = Bs.data.t()
+    resid = (L @ X - Bsd).abs().max().item()
+    eta = resid / (L.abs().sum(1).max().item() * max(X.abs().max().item(), Bsd.abs().max().item(), 1.0)
+                   * n * np.finfo(float).eps)
+    finite = bool(torch.isfinite(X).all().item())
+    eta = allmax(eta if finite else float("inf"), world)
+    del L, X, A, B, Bs
+    torch.cuda.empty_cache()
+    value = float(n) * n * m_total / (ms * 1e-3) / 1e9
+    log(f"c5: {value:.1f} GFLOP/s over {world} GPU(s), {ms:.2f} ms/step, eta {eta:.3e}")
+    return {"value": value, "unit": "GFLOP/s", "ms_per_step": ms, "steps": args.c5_steps, "n_gpus": world,
+            "scaling": "strong", "clocks": clk.summary(),
+            "workload": f"C5: TRSM Left/Lower/NoTrans/NonUnit fp64 n={n}, m={m_total} total, {m} per GPU, "
+                        "A broadcast from rank 0 inside every step",
+            "residual": {"eta": eta, "finite": eta != float("inf"), "bound": 32, "columns_per_rank": 8}}
+
+
 # ----------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -225,15 +379,22 @@ def main():
     ap.add_argument("--no-fp32", action="store_true")
     ap.add_argument("--threshold", type=int, default=256)
     ap.add_argument("--op-headline", choices=["trsm", "trmm"], default="trsm")
-    ap.add_argument("--ref-cols", type=int, default=256)
+    ap.add_argument("--ref-cols", type=int, default=1024,
+                    help="column slice of the reference arm and of cpu_baseline (the same slice)")
     ap.add_argument("--ref-threshold", type=int, default=256)
-    ap.add_argument("--cpu-cols", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--no-trmm", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 strong-scaling line")
+    ap.add_argument("--c5-steps", type=int, default=3)
+    ap.add_argument("--dry-gloo", action="store_true",
+                    help="CPU-only plumbing check: spawn, gloo rendezvous, broadcast of A, max over ranks; no compute")
     args = ap.parse_args()
 
+    rc_spawn = spawn_ranks(args)
+    if rc_spawn is not None:
+        sys.exit(rc_spawn)
     world, rank, local = setup_dist(args)
     if args.config == "c5":
         args.n = args.n or 8192
@@ -243,11 +404,15 @@ def main():
         args.n = args.n or 16384
         args.m = args.m or 16384
         args.scaling = "weak"
+    if args.dry_gloo:
+        run_dry(args, world, rank)
+        return
     if args.impl == "reference":
         run_reference(args, world, rank)
-        if world > 1:
+        if dist.is_initialized():
             dist.destroy_process_group()
         return
+    cpu_affinity = bind_to_gpu_numa_node(local)
 
     import paper_2504_13821_b200 as rc
     from paper_2504_13821_b200 import (ASYNC, TF32X3, Backend, Diag, MatrixBuffer, Side, Threshold, Trans,
@@ -270,7 +435,7 @@ def main():
     if rank == 0:
         rc.make_dominant(A_trsm.view(), Uplo.Lower)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist.is_initialized():
         dist.broadcast(A.data, src=0)
     be = Backend.cuda(device=local, stream=stream, flags=ASYNC)
 
@@ -284,7 +449,7 @@ def main():
         Abuf = Abuf if Abuf is not None else A
         Bbuf = Bbuf if Bbuf is not None else B
         fn = rc.rec_trsm if op == "trsm" else rc.rec_trmm
-        if world > 1:
+        if dist.is_initialized():
             dist.broadcast(Abuf.data, src=0)
         fn(specs[op], Abuf.cview(), Bbuf.view(), Threshold(args.threshold), backend or be)
 
@@ -417,7 +582,14 @@ def main():
         "per_launch_flops": g["flops"] / max(g["launches"], 1), "launches": g["launches"],
         "share_of_step": g["ms"] / step_ms_prof if step_ms_prof else None,
         "breakdown_ms": {k: v["ms"] for k, v in prof.items()},
+        "achieved_source": "per-launch CUDA events on the launching stream in one untimed step with direct "
+                           "launches on one stream (the profiling mode of the library)",
     }
+    # The same GEMM flops inside the TIMED configuration (graph, 2 right-hand-side
+    # streams): the step time minus the non-GEMM kernels' profiled time.
+    other_ms = step_ms_prof - g["ms"]
+    roofline["achieved_in_step"] = g["flops"] / max((ms_step - other_ms) * 1e-3, 1e-9) / 1e12
+    roofline["frac_in_step"] = roofline["achieved_in_step"] / peak64 if peak64 > 0 else None
     # The leaf (trsm_base per diagonal block): achieved HBM bandwidth on its
     # algorithmic bytes (nb(nb+1)/2 + 2 nb r) * 8 next to the
     # measured copy bandwidth -- it is latency / tensor bound, not HBM bound.
@@ -488,9 +660,20 @@ def main():
             cublas = cublas_compare(A, B0, n, m, args)
         except Exception as e:  # pragma: no cover
             cublas = {"error": str(e)}
+    # Second roofline denominator: cuBLAS DGEMM (16384^3) measured in this run.
+    dg = (cublas or {}).get("dgemm", {}).get("tflops_2n3")
+    if dg:
+        roofline["peak_cublas_dgemm"] = dg
+        roofline["frac_vs_cublas_dgemm"] = roofline["achieved"] / dg
+        roofline["achieved_in_step_frac_vs_cublas_dgemm"] = roofline["achieved_in_step"] / dg
+
+    c5 = None
+    if not args.no_c5 and args.config != "c5":
+        c5 = run_c5(args, world, rank, local, rc, stream)
 
     cpu = None
     if not args.no_cpu_baseline and world == 1 and rank == 0:
+        os.sched_setaffinity(0, cpu_affinity)  # every host core, like the reference arm
         cpu = cpu_baseline(args)
 
     if rank == 0:
@@ -502,11 +685,12 @@ def main():
             "pct_of_peak": value / 1e3 / (peak64 * world) * 100,
             "residual": {"eta": eta, "finite": finite, "bound": 32,
                          "definition": "||tril(A) X - B||_max / (||A||_inf max(|X|,|B|,1) n eps), 8 sampled columns"},
-            "trmm": trmm, "fp32": fp32, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "cublas": cublas,
+            "trmm": trmm, "fp32": fp32, "c5_strong": c5, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "cublas": cublas,
             "clocks": clocks, "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
@@ -555,22 +739,29 @@ def cublas_strsm(A32, B32_0, n, m):
 
 
 def cpu_baseline(args):
-    """The reference's CPU path (oracle/_ref) on the host cores, bounded sample."""
+    """The reference's CPU path (oracle/_ref) on the host cores, bounded
+    sample: the same column slice, generator, threshold and statistic (median
+    of repeated calls) as the `--impl reference` arm."""
     import oracle
     from oracle import ref
 
-    n, m_s = args.n, args.cpu_cols
+    n, m_s = args.n, args.ref_cols
     a, b = make_host_inputs(n, m_s, "trsm")
     spec = oracle.spec(0, 0, 0, 0, 1.0)
     if ref.available():
-        ref.rec("trsm", spec, a, b[:, :16].copy(order="F"), 256, width=-1)  # warm
-        t0 = time.perf_counter()
-        st, _, _, _ = ref.rec("trsm", spec, a, b, 256, width=-1)
-        t = time.perf_counter() - t0
-        assert st == 0
+        reps = 3
+        ref.rec("trsm", spec, a, b[:, :16].copy(order="F"), args.ref_threshold, width=-1)  # warm
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            st, _, _, _ = ref.rec("trsm", spec, a, b, args.ref_threshold, width=-1)
+            ts.append(time.perf_counter() - t0)
+            assert st == 0
+        t = statistics.median(ts)
         return {"value": n * n * m_s / t / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "reference",
-                "sample": f"rec_trsm left-lower-n-nonunit fp64 n={n}, m={m_s} column slice, threshold 256, "
-                          f"Backend::par() ({os.cpu_count()} threads), one call ({t:.1f} s)"}
+                "sample": f"rec_trsm left-lower-n-nonunit fp64 n={n}, m={m_s} column slice (the reference arm's), "
+                          f"threshold {args.ref_threshold}, Backend::par() ({os.cpu_count()} threads), "
+                          f"median of {reps} calls ({t:.2f} s each)"}
     m_s = 4
     t0 = time.perf_counter()
     oracle.oracle_trsm(spec, a, b[:, :m_s].copy(order="F"))

@@ -28,3 +28,19 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert "workload" in d["config"]
+
+
+def test_gpus_flag_spawns_ranks_dry_gloo():
+    """`bench.py --gpus 2` outside torchrun launches 2 ranks itself (the
+    driver's `--gpus N` form), rendezvous on 127.0.0.1, broadcasts A from rank
+    0 and takes the max over ranks -- here on gloo, with no compute."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-gloo", "--steps", "2",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"] and d["broadcast_ok"] and d["backend"] == "gloo"
+    assert d["value"] is None  # nothing computed: no number is claimed
+    assert d["config"]["m_total"] == 2 * d["config"]["m_per_gpu"]
+    assert "rank 0 of 2" in r.stderr and "rank 1 of 2" in r.stderr
