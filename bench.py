@@ -133,11 +133,17 @@ def setup_dist(args):
         if args.dry_gloo:
             dist.init_process_group("gloo")
         else:
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+            nccl_log = None
+            if "NCCL_DEBUG" not in os.environ:  # communicator INIT lines, echoed to stderr below
+                nccl_log = f"/tmp/rectri_bench_nccl.{os.getpid()}.log"
+                os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT", NCCL_DEBUG_FILE=nccl_log)
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+            if nccl_log and os.path.exists(nccl_log):
+                for ln in Path(nccl_log).read_text().splitlines():
+                    if "nRanks" in ln or "Init COMPLETE" in ln or "NCCL version" in ln:
+                        log("nccl: " + ln.strip())
         log(f"bench: rank {dist.get_rank()} of {dist.get_world_size()} ({dist.get_backend()}), local rank {local}")
         if args.gpus != world:
             log(f"bench: note --gpus {args.gpus} but WORLD_SIZE {world}; the launcher's world size is used")
@@ -353,7 +359,7 @@ def run_c5(args, world, rank, local, rc, stream):
     eta = resid / (L.abs().sum(1).max().item() * max(X.abs().max().item(), Bsd.abs().max().item(), 1.0)
                    * n * np.finfo(float).eps)
     finite = bool(torch.isfinite(X).all().item())
-    eta = allmax(eta if finite else float("inf"), world)
+    eta = float(allmax(float(eta) if finite else float("inf"), world))
     del L, X, A, B, Bs
     torch.cuda.empty_cache()
     value = float(n) * n * m_total / (ms * 1e-3) / 1e9

@@ -161,8 +161,20 @@ const char* rectri_cu_last_error(void);
 int64_t rectri_cu_launch_count(void);
 
 /* Drops every cached CUDA graph (e.g. before freeing buffers whose
- * addresses are baked into cached graphs). */
+ * addresses are baked into cached graphs).  The cache is bounded by entry
+ * count (64) and by the device bytes its entries own
+ * (RECTRI_CU_GRAPH_CACHE_MB, default 4096).  Deferred singularity checks of
+ * RECTRI_CU_ASYNC calls survive and are reported by rectri_cu_sync. */
 void rectri_cu_clear_graph_cache(void);
+
+/* Frees the per-device staging buffers of the host-operand path (they grow
+ * to the largest host-resident problem seen and are otherwise kept for
+ * reuse).  Waits for a host-operand call in flight on that device. */
+void rectri_cu_release_staging(void);
+
+/* Device bytes the library currently holds across calls: cached graphs'
+ * scratch plus staging buffers. */
+int64_t rectri_cu_device_bytes_held(void);
 
 int rectri_cu_abi_version(void);
 

@@ -77,6 +77,8 @@ SIGNATURES = {
     "rectri_cu_last_error": (ctypes.c_char_p, []),
     "rectri_cu_launch_count": (c_i64, []),
     "rectri_cu_clear_graph_cache": (None, []),
+    "rectri_cu_release_staging": (None, []),
+    "rectri_cu_device_bytes_held": (c_i64, []),
     "rectri_cu_abi_version": (ctypes.c_int, []),
     "rectri_cu_fill_uniform": (ctypes.c_int, [c_i32, View, c_i64, c_i64, ctypes.c_uint64, _P(BackendC)]),
     "rectri_cu_make_dominant": (ctypes.c_int, [c_i32, View, c_i32, _P(BackendC)]),

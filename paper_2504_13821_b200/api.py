@@ -557,6 +557,16 @@ def clear_graph_cache() -> None:
     _lib.load().rectri_cu_clear_graph_cache()
 
 
+def release_staging() -> None:
+    """Frees the host-operand path's device staging buffers."""
+    _lib.load().rectri_cu_release_staging()
+
+
+def device_bytes_held() -> int:
+    """Device bytes held across calls (cached graphs' scratch + staging)."""
+    return int(_lib.load().rectri_cu_device_bytes_held())
+
+
 # ---------------------------------------------------------------------------
 # Utilities (not reference entry points): device-side synthetic inputs, peak
 # probe and per-kernel-class profiling.

@@ -523,6 +523,10 @@ struct DeviceRes {
   static constexpr int kSlots = 3;            // 0: A, 1..2: B panels
   void* stage[kSlots] = {nullptr, nullptr, nullptr};
   size_t stage_bytes[kSlots] = {0, 0, 0};
+  // Held for a whole host-operand call: the staging buffers (and the copy
+  // streams) serve one call at a time, and are never reallocated or released
+  // under a call that is still using them.
+  std::mutex stage_mu;
 };
 
 std::mutex g_mu;
@@ -585,10 +589,16 @@ struct GraphEntry {
   double* packed = nullptr;  // fp64 leaf triangles, packed once per call
   void* leaf_meta = nullptr;  // their row offsets and orders
   void* conc_scratch = nullptr;  // concurrent TRMM nodes' GEMM products
+  CallScratch scratch;           // unpacked-leaf and 3xTF32 split buffers of the captured kernels
+  size_t bytes = 0;              // device bytes this entry owns (graph-cache byte cap)
   i64 nodes = 0;
   int device = 0;
   ~GraphEntry() {
     if (exec) cudaGraphExecDestroy(exec);
+    for (int k = 0; k < scratch.n; ++k) {
+      if (scratch.leaf[k]) cudaFree(scratch.leaf[k]);
+      if (scratch.split[k]) cudaFree(scratch.split[k]);
+    }
     if (packed) cudaFree(packed);
     if (leaf_meta) cudaFree(leaf_meta);
     if (conc_scratch) cudaFree(conc_scratch);
@@ -600,10 +610,23 @@ struct GraphEntry {
 using Key = std::tuple<int, int, int, int, int, int, uint64_t, const void*, i64, i64, void*, i64,
                        i64, i64, i64, int>;
 
+// LRU of captured calls, bounded by entry count AND by the device bytes the
+// entries own (packed leaf triangles, TRMM scratch, graph-owned leaf/split
+// scratch): RECTRI_CU_GRAPH_CACHE_MB (default 4096).  The newest entry is
+// always kept.  Entries are shared_ptr: an evicted entry still referenced by
+// a pending ASYNC call lives until that call is synced.
 struct Cache {
   std::list<std::pair<Key, std::shared_ptr<GraphEntry>>> lru;
   std::map<Key, decltype(lru)::iterator> index;
   static constexpr size_t kCap = 64;
+  size_t bytes = 0;
+  static size_t byte_cap() {
+    static const size_t cap = [] {
+      const char* e = getenv("RECTRI_CU_GRAPH_CACHE_MB");
+      return (e && atoll(e) > 0 ? static_cast<size_t>(atoll(e)) : size_t{4096}) << 20;
+    }();
+    return cap;
+  }
   std::shared_ptr<GraphEntry> get(const Key& k) {
     auto it = index.find(k);
     if (it == index.end()) return nullptr;
@@ -611,22 +634,36 @@ struct Cache {
     return it->second->second;
   }
   void put(const Key& k, std::shared_ptr<GraphEntry> e) {
+    bytes += e->bytes;
     lru.emplace_front(k, std::move(e));
     index[k] = lru.begin();
-    while (lru.size() > kCap) {
+    bool evicted = false;
+    while (lru.size() > 1 && (lru.size() > kCap || bytes > byte_cap())) {
+      bytes -= lru.back().second->bytes;
       index.erase(lru.back().first);
+      // replays of an evicted graph may still be in flight on some stream:
+      // finish them before its memory and executable are released
+      if (!evicted) cudaDeviceSynchronize();
+      evicted = true;
       lru.pop_back();
     }
   }
   void clear() {
+    if (!lru.empty()) cudaDeviceSynchronize();
     index.clear();
     lru.clear();
+    bytes = 0;
   }
 };
 Cache g_cache;
 
-// Pending singularity checks for RECTRI_CU_ASYNC calls, per stream.
+// Pending singularity checks for RECTRI_CU_ASYNC calls, per stream.  At most
+// kMaxPending per stream: beyond that the stream is synchronized and the
+// checks settled early, the first singular row kept in g_deferred until the
+// caller's rectri_cu_sync reports it.
 std::multimap<cudaStream_t, std::shared_ptr<GraphEntry>> g_pending;
+std::map<cudaStream_t, i64> g_deferred;
+constexpr size_t kMaxPending = 256;
 
 struct DeviceGuard {
   int prev = -1;
@@ -680,6 +717,7 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
       }
       cuda_check(cudaMalloc(&g->packed, static_cast<size_t>(nleaves) * leaf3_scratch_doubles() * sizeof(double)),
                  "leaf pack alloc");
+      g->bytes += static_cast<size_t>(nleaves) * leaf3_scratch_doubles() * sizeof(double);
       cuda_check(cudaMalloc(&g->leaf_meta, static_cast<size_t>(nleaves) * (sizeof(long long) + sizeof(int))),
                  "leaf meta alloc");
       long long* d_r0 = static_cast<long long*>(g->leaf_meta);
@@ -728,6 +766,7 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
         resp = &device_res(dev);
       }
       cuda_check(cudaMalloc(&g->conc_scratch, static_cast<size_t>(need) * sizeof(T)), "trmm scratch alloc");
+      g->bytes += static_cast<size_t>(need) * sizeof(T);
       conc.streams = capture ? &resp->conc_streams : &resp->conc_streams_dir;
       conc.scratch = static_cast<T*>(g->conc_scratch);
       conc.cap = need;
@@ -735,18 +774,36 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
   }
   i64& counter = launch_counter();
   const i64 before = counter;
+  struct ScratchScope {  // the graph's own scratch for the launchers, during the capture only
+    explicit ScratchScope(const CallScratch* cs) { set_call_scratch(cs); }
+    ~ScratchScope() { set_call_scratch(nullptr); }
+  };
+  std::unique_ptr<ScratchScope> scratch_scope;
   if (capture) {
-    // per-stream leaf scratch must exist before capture (no allocation inside)
+    // Scratch of the kernels captured on each stream (s and the panel
+    // streams), owned by this graph and allocated before the capture.
     DeviceRes& res = device_res(dev);  // the capture path holds g_mu
-    leaf_scratch_reserve(s);
-    for (cudaStream_t a : res.aux) leaf_scratch_reserve(a);
-    if (std::is_same<T, float>::value && tf32x3_enabled()) {
-      // 3xTF32 operand splits: hi + lo of the largest off-diagonal block and source half
-      const i64 n = A.rows, h = n - n / 2, rhs = spec.side == RECTRI_CU_LEFT ? B.cols : B.rows;
-      const size_t need = 2 * static_cast<size_t>(h * h + h * rhs);
-      tf32x3_reserve(s, need);
-      for (cudaStream_t a : res.aux) tf32x3_reserve(a, need);
+    const bool leaf_scratch = nleaves == 0 && leaf_version() >= 2;
+    const bool split = std::is_same<T, float>::value && tf32x3_enabled();
+    // 3xTF32 operand splits: hi + lo of the largest off-diagonal block and source half
+    const i64 h = A.rows - A.rows / 2;
+    const i64 pw = P_ <= 1 ? rhs_ : ((rhs_ + P_ - 1) / P_ + 63) / 64 * 64;  // a stream's panel
+    const size_t split_need = 2 * static_cast<size_t>(h * h + h * std::min(pw, rhs_));
+    CallScratch& cs = g->scratch;
+    for (int k = 0; k < P_ && (leaf_scratch || split); ++k) {
+      cs.stream[k] = k == 0 ? s : res.aux[k - 1];
+      cs.n = k + 1;
+      if (leaf_scratch) {
+        cuda_check(cudaMalloc(&cs.leaf[k], leaf_scratch_bytes()), "leaf scratch alloc");
+        g->bytes += leaf_scratch_bytes();
+      }
+      if (split) {
+        cuda_check(cudaMalloc(&cs.split[k], split_need * sizeof(float)), "3xTF32 scratch alloc");
+        cs.split_floats[k] = split_need;
+        g->bytes += split_need * sizeof(float);
+      }
     }
+    scratch_scope = std::make_unique<ScratchScope>(&g->scratch);
     cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
   }
   if (op == kTrsm && spec.alpha != 1.0) {
@@ -932,8 +989,26 @@ void run_device(OpK op, const Spec& spec, DView<const T> A, DView<T> B, i64 thre
       enqueue_device<T>(op, spec, A, B, threshold, be.stream, be.flags, sink, user, dev);
   if (async) {
     if (g->h_flags) {
-      std::lock_guard<std::mutex> lock(g_mu);
-      g_pending.emplace(be.stream, g);
+      std::vector<std::shared_ptr<GraphEntry>> settle;
+      {
+        std::lock_guard<std::mutex> lock(g_mu);
+        g_pending.emplace(be.stream, g);
+        if (g_pending.count(be.stream) > kMaxPending) {
+          auto range = g_pending.equal_range(be.stream);
+          for (auto it = range.first; it != range.second; ++it) settle.push_back(it->second);
+          g_pending.erase(be.stream);
+        }
+      }
+      if (!settle.empty()) {
+        cuda_check(cudaStreamSynchronize(be.stream), "synchronize");
+        i64 r = -1;
+        for (const auto& e : settle)
+          if (r < 0) r = first_singular(*e);
+        if (r >= 0) {
+          std::lock_guard<std::mutex> lock(g_mu);
+          g_deferred.emplace(be.stream, r);  // keeps the earliest
+        }
+      }
     }
     return;
   }
@@ -1422,7 +1497,12 @@ void rec_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
   {
     std::lock_guard<std::mutex> lock(g_mu);
     res = &device_res(dev);
-    if (!a_dev) dA = DView<const T>{static_cast<T*>(staging(*res, 0, static_cast<size_t>(n * n) * sizeof(T))), n, n, n};
+  }
+  // one host-operand call per device at a time owns the staging buffers
+  std::lock_guard<std::mutex> stage_lock(res->stage_mu);
+  if (!a_dev) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    dA = DView<const T>{static_cast<T*>(staging(*res, 0, static_cast<size_t>(n * n) * sizeof(T))), n, n, n};
   }
   BackendInfo be2 = be;
   be2.flags &= ~RECTRI_CU_ASYNC;
@@ -1671,11 +1751,22 @@ int rectri_cu_sync(void* stream, int64_t* singular_row) {
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         cuda_check(cudaStreamSynchronize(s), "synchronize");
         std::vector<std::shared_ptr<GraphEntry>> pend;
+        i64 deferred = -1;
         {
           std::lock_guard<std::mutex> lock(g_mu);
           auto range = g_pending.equal_range(s);
           for (auto it = range.first; it != range.second; ++it) pend.push_back(it->second);
           g_pending.erase(s);
+          auto d = g_deferred.find(s);
+          if (d != g_deferred.end()) {
+            deferred = d->second;
+            g_deferred.erase(d);
+          }
+        }
+        if (deferred >= 0) {
+          Fail f{RECTRI_CU_SINGULAR, "singular triangular matrix: zero diagonal at row " + std::to_string(deferred)};
+          f.index = deferred;
+          throw f;
         }
         for (const auto& g : pend) {
           const i64 r = first_singular(*g);
@@ -1695,9 +1786,40 @@ const char* rectri_cu_last_error(void) { return g_last_error.c_str(); }
 int64_t rectri_cu_launch_count(void) { return launch_counter(); }
 
 void rectri_cu_clear_graph_cache(void) {
+  // Pending ASYNC checks keep their entries alive (shared_ptr) and are still
+  // reported by the next rectri_cu_sync on their stream.
   std::lock_guard<std::mutex> lock(g_mu);
-  g_pending.clear();
   g_cache.clear();
+}
+
+void rectri_cu_release_staging(void) {
+  std::vector<std::pair<int, DeviceRes*>> devs;  // map nodes are stable
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (auto& kv : g_dev) devs.push_back({kv.first, &kv.second});
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (auto& d : devs) {
+    DeviceRes& r = *d.second;
+    std::lock_guard<std::mutex> stage_lock(r.stage_mu);  // waits for a host-operand call in flight
+    std::lock_guard<std::mutex> lock(g_mu);
+    cudaSetDevice(d.first);
+    for (int k = 0; k < DeviceRes::kSlots; ++k) {
+      if (r.stage[k]) cudaFree(r.stage[k]);
+      r.stage[k] = nullptr;
+      r.stage_bytes[k] = 0;
+    }
+  }
+  cudaSetDevice(prev);
+}
+
+int64_t rectri_cu_device_bytes_held(void) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  size_t b = g_cache.bytes;
+  for (auto& kv : g_dev)
+    for (int k = 0; k < DeviceRes::kSlots; ++k) b += kv.second.stage_bytes[k];
+  return static_cast<int64_t>(b);
 }
 
 int rectri_cu_abi_version(void) { return RECTRI_CU_ABI_VERSION; }

@@ -104,4 +104,28 @@ double probe_peak_tflops(int kind);
 // Number of kernel launches issued (incremented by each launcher).
 i64& launch_counter();
 
+// Scratch a captured graph owns, by the stream its kernels are captured on:
+// the unpacked-leaf scratch (leaf64.cu) and the 3xTF32 operand splits
+// (sgemm_tf32x3.cu).  While a graph is being captured the builder installs
+// its set for the capturing thread, and the launchers take their buffers from
+// it instead of the per-stream pools -- so a cached graph never shares
+// scratch with another graph (two replays on different streams may run at
+// once) and never points at a pool buffer that is later reallocated.
+struct CallScratch {
+  static constexpr int kMax = 8;
+  int n = 0;
+  cudaStream_t stream[kMax] = {};
+  double* leaf[kMax] = {};
+  float* split[kMax] = {};
+  size_t split_floats[kMax] = {};
+  int find(cudaStream_t s) const {
+    for (int k = 0; k < n; ++k)
+      if (stream[k] == s) return k;
+    return -1;
+  }
+};
+void set_call_scratch(const CallScratch* cs);  // thread-local; nullptr to clear
+const CallScratch* call_scratch();
+size_t leaf_scratch_bytes();  // one stream's unpacked-leaf scratch
+
 }  // namespace rectri_cu

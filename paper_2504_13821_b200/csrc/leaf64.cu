@@ -437,6 +437,10 @@ std::mutex g_mu;
 std::map<std::pair<int, cudaStream_t>, double*> g_scratch;
 
 double* scratch_for(cudaStream_t s, bool may_alloc) {
+  if (const CallScratch* cs = call_scratch()) {  // a graph capture: the graph's own buffer
+    const int k = cs->find(s);
+    return k >= 0 ? cs->leaf[k] : nullptr;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(g_mu);
@@ -478,6 +482,14 @@ void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s) {
 }
 
 void leaf_scratch_reserve(cudaStream_t s) { leaf64::scratch_for(s, true); }
+
+size_t leaf_scratch_bytes() { return leaf64::kScratchDoubles * sizeof(double); }
+
+namespace {
+thread_local const CallScratch* t_call_scratch = nullptr;
+}
+void set_call_scratch(const CallScratch* cs) { t_call_scratch = cs; }
+const CallScratch* call_scratch() { return t_call_scratch; }
 
 void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s) {
   using namespace leaf64;

@@ -329,6 +329,10 @@ struct Scratch {
 std::map<std::pair<int, cudaStream_t>, Scratch> g_scratch;
 
 float* scratch(cudaStream_t s, size_t floats) {
+  if (const CallScratch* cs = call_scratch()) {  // a graph capture: the graph's own buffer
+    const int k = cs->find(s);
+    return k >= 0 && cs->split_floats[k] >= floats ? cs->split[k] : nullptr;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(g_mu);
