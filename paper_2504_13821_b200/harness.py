@@ -166,27 +166,32 @@ def validate_result(op: OpKind, spec: TriangularSpec, a: torch.Tensor, b_orig: t
 
 
 def _cublas_call(op, spec, n, m, A, B):
+    """cuBLAS ?trsm / ?trmm (tools/libcublas_cmp.so) on the same device
+    buffers, every side/uplo/trans/diag variant (ConjTrans == Trans on reals).
+    trmm is out of place in cuBLAS: its result is copied back into B (outside
+    the timed call).  Returns a callable giving the call's time in ms."""
     lib = ctypes.CDLL(str(Path(__file__).resolve().parents[1] / "tools" / "libcublas_cmp.so"))
-    if Side(spec.side) != Side.Left or Trans(spec.trans) != Trans.NoTrans or Diag(spec.diag) != Diag.NonUnit:
-        raise ConfigError("cublas backend: only left-*-n-nonunit variants are wired")
-    sfx = "d" if A.dtype == torch.float64 else "s"
-    if op == OpKind.Trsm and Uplo(spec.uplo) == Uplo.Lower:
-        f = getattr(lib, f"cmp_{sfx}trsm_lln")
-        f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    dtype = 1 if A.dtype == torch.float64 else 0
+    side, uplo = int(Side(spec.side)), int(Uplo(spec.uplo))
+    trans = 0 if Trans(spec.trans) == Trans.NoTrans else 1
+    diag = int(Diag(spec.diag))
+    rows, cols = (n, m) if side == 0 else (m, n)
+    if op == OpKind.Trsm:
+        f = lib.cmp_trsm
+        f.argtypes = [i32, i32, i32, i32, i32, vp, i64, vp, i64, i64, i32]
         f.restype = ctypes.c_double
-        return lambda: f(A.data_ptr(), n, B.data_ptr(), m, 1)
-    if op == OpKind.Trmm and Uplo(spec.uplo) == Uplo.Upper:
-        out = torch.empty_like(B)
-        f = getattr(lib, f"cmp_{sfx}trmm_lun")
-        f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]
-        f.restype = ctypes.c_double
+        return lambda: f(dtype, side, uplo, trans, diag, A.data_ptr(), n, B.data_ptr(), rows, cols, 1)
+    out = torch.empty_like(B)
+    f = lib.cmp_trmm
+    f.argtypes = [i32, i32, i32, i32, i32, vp, i64, vp, vp, i64, i64, i32]
+    f.restype = ctypes.c_double
 
-        def run():
-            t = f(A.data_ptr(), n, B.data_ptr(), out.data_ptr(), m, 1)
-            B.copy_(out)
-            return t
-        return run
-    raise ConfigError("cublas backend: only trsm left-lower and trmm left-upper are wired")
+    def run():
+        t = f(dtype, side, uplo, trans, diag, A.data_ptr(), n, B.data_ptr(), out.data_ptr(), rows, cols, 1)
+        B.copy_(out)
+        return t
+    return run
 
 
 def time_one(config: BenchConfig, n: int, m: int, seed: int) -> BenchRecord:

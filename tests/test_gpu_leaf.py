@@ -127,3 +127,42 @@ def test_leaf_v3_panel_widths_bitwise(cuda, monkeypatch, dt, op, side, uplo, tra
         check_against_oracle(op, s, a, b, outs[0])
         for k, o in enumerate(outs[1:], 1):
             assert oracle.bitwise_equal(outs[0], o), (n, m, k)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("op", ["trsm", "trmm"])
+@pytest.mark.parametrize("width", [8, 16, 32])
+def test_default_leaf_replay_stress(cuda, monkeypatch, op, dtype, width):
+    """Ring-ordering stress of the DEFAULT leaves (leaf3_kernel / leaf32_kernel:
+    a producer warp refills mbarrier-guarded bulk-copy slots while 4-8 compute
+    warps read them -- the ordering compute-sanitizer racecheck cannot model).
+    A refill racing a slot's readers shows up as run-to-run differences (it
+    caught a real one: tools/leaf3_stress.py): 24 graph replays of the same
+    recursion must be bitwise identical, and within the oracle tolerance
+    (the reference's own role for the workgroup simulator's race detector,
+    src/workgroup.cpp:138-177, tests/test_workgroup.cpp:144-176)."""
+    import paper_2504_13821_b200 as rc
+    import torch
+
+    monkeypatch.setenv("RECTRI_CU_LEAF", "3")
+    monkeypatch.setenv("RECTRI_CU_LEAF_NC", str(width))
+    rc.clear_graph_cache()  # the panel width is fixed at capture
+    rng = np.random.default_rng(300 + width)
+    n, m = 1024, 2304
+    s = oracle.spec(0, 0, 0, 0, 1.0)
+    a, b = _inputs(op, s, n, m, rng)
+    a, b = F(a.astype(dtype)), F(b.astype(dtype))
+    A, B = to_dev(a), to_dev(b)
+    B0 = B.data.clone()
+    fn = rec_trmm if op == "trmm" else rec_trsm
+    first = None
+    for rep in range(24):
+        B.data.copy_(B0)
+        fn(tspec(s), A.cview(), B.view(), Threshold(256), Backend.cuda())
+        torch.cuda.synchronize()
+        if first is None:
+            first = B.data.clone()
+            check_against_oracle(op, s, a, b, to_np(B))
+        else:
+            assert torch.equal(B.data, first), (op, width, rep)
+    rc.clear_graph_cache()

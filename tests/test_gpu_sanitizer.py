@@ -47,3 +47,19 @@ def test_planted_race_is_detected(cuda):
     out = r.stdout + r.stderr
     m = re.search(r"RACECHECK SUMMARY: (\d+) hazards displayed \((\d+) errors", out)
     assert m and int(m.group(1)) > 0 and int(m.group(2)) > 0, out[-3000:]
+
+
+@pytest.mark.parametrize("tool", ["synccheck", "initcheck"])
+@pytest.mark.parametrize("args", [["leaf", "256", "16384"], ["leaf", "256", "3000"], ["leaf", "256", "1000"],
+                                  ["trmmleaf", "256", "16384"], ["leaf32", "256", "16384"],
+                                  ["leaf32", "256", "1000"], ["trsm", "1024", "4096", "256"]])
+def test_default_leaves_at_c3_leaf_shape(cuda, tool, args):
+    """The DEFAULT leaves (leaf3_kernel, fp64; leaf32_kernel, fp32) at the C3
+    leaf shape (256 x 16384: 32-wide panels) and at the 16- / 8-wide panel
+    widths: barrier use (synccheck) and no read of uninitialised device
+    memory (initcheck).  Their ring ordering -- which racecheck cannot model
+    -- is covered by test_gpu_leaf.py's replay-determinism stress test."""
+    r = _san(tool, args)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-3000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-3000:]

@@ -78,3 +78,25 @@ def test_gpu_sweep_and_fault_gate(cuda, tmp_path):
                               "--elem", "f32", "--reps", "2", "--warmup", "1"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert len(r.stdout.splitlines()) == 3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("op", ["trsm", "trmm"])
+def test_gpu_cublas_backend_every_variant(cuda, tmp_path, op):
+    """The cuBLAS comparison backend covers all 16 variants (the gate checks
+    its results too), so the Fig.-3-style ratio report can join any variant."""
+    import itertools
+
+    for side, uplo, trans, diag in itertools.product(("left", "right"), ("lower", "upper"), ("n", "t"),
+                                                     ("nonunit", "unit")):
+        outs = {}
+        for backend in ("cuda", "cublas"):
+            out = tmp_path / f"{op}-{side}-{uplo}-{trans}-{diag}-{backend}.csv"
+            r = subprocess.run(CLI + ["sweep", "--op", op, "--side", side, "--uplo", uplo, "--trans", trans,
+                                      "--diag", diag, "--sizes", "96", "--m", "fixed:40", "--threshold", "32",
+                                      "--backend", backend, "--reps", "2", "--warmup", "1", "--elem", "f64",
+                                      "--out", str(out)], capture_output=True, text=True)
+            assert r.returncode == 0, (side, uplo, trans, diag, backend, r.stderr)
+            outs[backend] = out
+        recs = h.ratio_report(str(outs["cublas"]), str(outs["cuda"]))
+        assert len(recs) == 1 and recs[0].ratio_percent > 0

@@ -77,4 +77,47 @@ double cmp_sgemm(const float* A, const float* B, float* C, int64_t n, int reps) 
   return timed([&] { cublasSgemm(handle(), CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, A, n, B, n, &zero, C, n); },
                reps);
 }
+
+// Any variant (0/1 flags as rectri_cu_spec: side 0 Left, uplo 0 Lower, trans
+// 0 N / 1 T, diag 0 NonUnit; dtype 1 = f64, 0 = f32).  B is rows x cols
+// (ld = rows); A is rows x rows (Left) or cols x cols (Right), ld lda.
+// trsm solves in place; trmm is out of place (C = alpha op(A) B), ms.
+double cmp_trsm(int dtype, int side, int uplo, int trans, int diag, const void* A, int64_t lda, void* B,
+                int64_t rows, int64_t cols, int reps) {
+  const cublasSideMode_t sd = side ? CUBLAS_SIDE_RIGHT : CUBLAS_SIDE_LEFT;
+  const cublasFillMode_t ul = uplo ? CUBLAS_FILL_MODE_UPPER : CUBLAS_FILL_MODE_LOWER;
+  const cublasOperation_t tr = trans ? CUBLAS_OP_T : CUBLAS_OP_N;
+  const cublasDiagType_t dg = diag ? CUBLAS_DIAG_UNIT : CUBLAS_DIAG_NON_UNIT;
+  if (dtype == 1) {
+    const double one = 1.0;
+    return timed([&] {
+      cublasDtrsm(handle(), sd, ul, tr, dg, rows, cols, &one, static_cast<const double*>(A), lda,
+                  static_cast<double*>(B), rows);
+    }, reps);
+  }
+  const float one = 1.f;
+  return timed([&] {
+    cublasStrsm(handle(), sd, ul, tr, dg, rows, cols, &one, static_cast<const float*>(A), lda, static_cast<float*>(B),
+                rows);
+  }, reps);
+}
+double cmp_trmm(int dtype, int side, int uplo, int trans, int diag, const void* A, int64_t lda, const void* B,
+                void* C, int64_t rows, int64_t cols, int reps) {
+  const cublasSideMode_t sd = side ? CUBLAS_SIDE_RIGHT : CUBLAS_SIDE_LEFT;
+  const cublasFillMode_t ul = uplo ? CUBLAS_FILL_MODE_UPPER : CUBLAS_FILL_MODE_LOWER;
+  const cublasOperation_t tr = trans ? CUBLAS_OP_T : CUBLAS_OP_N;
+  const cublasDiagType_t dg = diag ? CUBLAS_DIAG_UNIT : CUBLAS_DIAG_NON_UNIT;
+  if (dtype == 1) {
+    const double one = 1.0;
+    return timed([&] {
+      cublasDtrmm(handle(), sd, ul, tr, dg, rows, cols, &one, static_cast<const double*>(A), lda,
+                  static_cast<const double*>(B), rows, static_cast<double*>(C), rows);
+    }, reps);
+  }
+  const float one = 1.f;
+  return timed([&] {
+    cublasStrmm(handle(), sd, ul, tr, dg, rows, cols, &one, static_cast<const float*>(A), lda,
+                static_cast<const float*>(B), rows, static_cast<float*>(C), rows);
+  }, reps);
+}
 }
