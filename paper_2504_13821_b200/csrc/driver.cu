@@ -292,7 +292,7 @@ void enqueue_gemm(T alpha, bool ta, DView<const T> A, bool tb, DView<const T> B,
 // internal recursion with the same schema (no events: semantically one call).
 template <typename T>
 void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s,
-                  double* packed = nullptr);
+                  double* packed = nullptr, int pack_asc = 0);
 
 // One kernel of the recursion, as emitted by a descriptor run (the streamed
 // host path executes these itself).
@@ -353,6 +353,7 @@ class Recursion {
   // (launch_leaf3_pack_all): leaf k reads packed + k * packed_stride.
   double* packed = nullptr;
   size_t packed_stride = 0;
+  int pack_asc = 0;  // TRMM triangles packed in ascending order (v4 leaf)
   int leaf_idx = 0;
   ConcCtx<T>* conc = nullptr;
 
@@ -373,7 +374,8 @@ class Recursion {
       if (leaves_) leaves_->push_back({row0, n});
       if (before) before(true, A, B, B);
       if (kernels) kernels(KDesc<T>{true, spec, A, B, B, T(0), false, false});
-      else if (!dry_) enqueue_base<T>(op_, spec, A, B, s_, packed ? packed + leaf_idx * packed_stride : nullptr);
+      else if (!dry_)
+        enqueue_base<T>(op_, spec, A, B, s_, packed ? packed + leaf_idx * packed_stride : nullptr, pack_asc);
       ++leaf_idx;
       return;
     }
@@ -481,7 +483,8 @@ LeafParams<T> leaf_params(OpK op, const Spec& spec, DView<const T> A, DView<T> B
 }
 
 template <typename T>
-void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s, double* packed) {
+void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s, double* packed,
+                  int pack_asc) {
   const i64 n = A.rows;
   const bool left = spec.side == RECTRI_CU_LEFT;
   const i64 rhs = left ? B.cols : B.rows;
@@ -506,6 +509,7 @@ void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaSt
   p.trsm = op == kTrsm ? 1 : 0;
   p.alpha = static_cast<T>(spec.alpha);
   p.packed = packed;
+  p.pack_asc = pack_asc;
   ProfScope prof(1, static_cast<double>(n) * n * rhs, s);
   K<T>::leaf(p, s);
 }
@@ -734,6 +738,12 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
       pbase.unit = spec.diag == RECTRI_CU_UNIT ? 1 : 0;
       pbase.trsm = op == kTrsm ? 1 : 0;
       pbase.alpha = static_cast<T>(eff.alpha);
+      // fp64 TRMM leaves of a stream panel this wide run the v4 kernel,
+      // which reads its triangles in ascending row order
+      const i64 rhs_all = spec.side == RECTRI_CU_LEFT ? B.cols : B.rows;
+      const int P0 = g_prof.on ? 1 : panel_streams(rhs_all);
+      const i64 w0 = P0 <= 1 ? rhs_all : ((rhs_all + P0 - 1) / P0 + 63) / 64 * 64;
+      pbase.pack_asc = std::is_same<T, double>::value && op == kTrmm && leaf4_use(w0) ? 1 : 0;
     }
   }
   // Concurrent TRMM nodes (ConcCtx): packed leaves only (no per-stream leaf
@@ -824,6 +834,7 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
     if (nleaves > 0) {
       r.packed = g->packed;
       r.packed_stride = leaf3_scratch_doubles();
+      r.pack_asc = pbase.pack_asc;
     }
     if (conc.scratch) r.conc = &conc;
     return r;
@@ -1282,6 +1293,14 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
       packs = static_cast<double*>(staging(*res, 2, leaves.size() * leaf3_scratch_doubles() * sizeof(double)));
     }
     std::vector<cudaEvent_t> packed_evs(units.size(), nullptr);
+    // TRMM triangles in the v4 leaf's ascending order when the first panel's
+    // stream parts are wide enough for it (the order is fixed for all panels)
+    int pack_asc = 0;
+    if (pack_once && op == kTrmm) {
+      const i64 prhs0 = std::min(rhs, tw);
+      const int P0 = panel_streams(prhs0);
+      pack_asc = leaf4_use(((prhs0 + P0 - 1) / P0 + 63) / 64 * 64) ? 1 : 0;
+    }
     for (int tp = 0; tp < TP && tp * tw < rhs; ++tp) {
       const i64 t0 = tp * tw, t1 = std::min(rhs, t0 + tw);
       // H2D in first-use order (A blocks in the first panel); ready[i] gates unit i.
@@ -1344,7 +1363,11 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
           if (tp == 0) {
             if (ready[i]) cuda_check(cudaStreamWaitEvent(ps[0], ready[i], 0), "wait input");
             if constexpr (std::is_same<T, double>::value)
-              launch_leaf3_pack(leaf_params<double>(op, k.spec, k.a, k.dst), packed, ps[0]);
+            {
+              LeafParams<double> lp = leaf_params<double>(op, k.spec, k.a, k.dst);
+              lp.pack_asc = pack_asc;
+              launch_leaf3_pack(lp, packed, ps[0]);
+            }
             packed_evs[i] = ev();
             cuda_check(cudaEventRecord(packed_evs[i], ps[0]), "record");
           }
@@ -1360,7 +1383,7 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
             }
           const DView<T> dst = rhs_part(u.dst, q);
           if (k.leaf) {
-            enqueue_base<T>(op, k.spec, k.a, dst, sq, packed);
+            enqueue_base<T>(op, k.spec, k.a, dst, sq, packed, pack_asc);
           } else if (k.off_on_left) {
             enqueue_gemm<T>(k.coeff, k.off_trans, u.a, false, rhs_part(k.src, q), T(1), dst, sq);
           } else {

@@ -48,6 +48,7 @@ struct LeafParams {
   int debug_skip = 0;
   long long* trace = nullptr;  // RECTRI_CU_LEAF_TRACE: per-CTA clock64 stamps (leaf64.cu)
   double* packed = nullptr;    // v3: this leaf's triangle already packed here (pack3_all_kernel)
+  int pack_asc = 0;            // packed TRMM blocks in ascending row order (the v4 leaf's; TRSM always is)
 };
 
 constexpr int kLeafMax = 256;
@@ -72,6 +73,10 @@ size_t leaf3_scratch_doubles();
 // Packs one leaf's triangle (p.A, p.n, variant flags) into dst.
 void launch_leaf3_pack(const LeafParams<double>& p, double* dst, cudaStream_t s);
 int leaf3_width(long long nrhs, bool trsm);  // fp64 leaf v3 panel width (8 / 16 / 32)
+// fp64 leaf v4 (leaf64_v4.cu): column-owning warps, bitwise the v3 arithmetic;
+// used (RECTRI_CU_LEAF >= 4, the default) for leaves with many right-hand sides.
+bool leaf4_use(long long nrhs);
+void launch_leaf_f64_v4(const LeafParams<double>& p, const double* packed, cudaStream_t s);
 int leaf_version();  // RECTRI_CU_LEAF (fp64: 1 = leaf.cu, 2 = leaf64.cu, 3 = leaf64_v3.cu)
 // Allocates the v2 fp64 leaf's per-stream scratch (call before capturing on s).
 void leaf_scratch_reserve(cudaStream_t s);

@@ -454,11 +454,13 @@ double* scratch_for(cudaStream_t s, bool may_alloc) {
 }
 
 int leaf_version_env() {
-  // 3 (default): explicit-inverse diagonal blocks as DMMA products
-  // (leaf64_v3.cu), ~2x faster leaves; 2: warp-shuffle substitution in the
-  // reference's order, bitwise equal to v1 (leaf.cu).
+  // 4 (default): explicit-inverse diagonal blocks as DMMA products, v4
+  // (leaf64_v4.cu, column-owning warps) for leaves with many right-hand
+  // sides and v3 (leaf64_v3.cu) for the others -- bitwise the same; 3: v3
+  // only; 2: warp-shuffle substitution in the reference's order, bitwise
+  // equal to v1 (leaf.cu).
   const char* e = getenv("RECTRI_CU_LEAF");
-  return e ? atoi(e) : 3;
+  return e ? atoi(e) : 4;
 }
 
 }  // namespace leaf64

@@ -83,7 +83,7 @@ __device__ void pack3_block(const LeafParams<double>& p, double* __restrict__ P,
   while ((I + 1) * (I + 2) / 2 <= b) ++I;
   const int J = b - I * (I + 1) / 2;
   const int r0 = I * kRB, j0 = J * kRB;
-  double* dst = P + static_cast<size_t>(seq_of(I, J, nblk, trsm)) * kBlk;
+  double* dst = P + static_cast<size_t>(seq_of(I, J, nblk, trsm || p.pack_asc)) * kBlk;
   const int tid = threadIdx.x;
   if (J < I) {
     for (int o = tid; o < kBlk; o += blockDim.x) {
@@ -413,9 +413,19 @@ void launch_leaf3_pack(const LeafParams<double>& p, double* dst, cudaStream_t s)
 void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream_t s, bool prepacked) {
   using namespace leaf64v3;
   const int nblk = (p.n + kRB - 1) / kRB;
-  if (!prepacked && (p.trsm || p.alpha != 0.0)) {
-    pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, scratch);
+  const bool zero = !p.trsm && p.alpha == 0.0;
+  // v4 (bitwise the same arithmetic) for many right-hand sides; a TRMM
+  // triangle packed in ascending order can only be consumed by v4.
+  const bool v4 = !zero && (prepacked ? (p.trsm ? leaf4_use(p.nrhs) : p.pack_asc != 0) : leaf4_use(p.nrhs));
+  if (!prepacked && !zero) {
+    LeafParams<double> q = p;
+    q.pack_asc = v4 ? 1 : 0;
+    pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(q, scratch);
     ++launch_counter();
+  }
+  if (v4) {
+    launch_leaf_f64_v4(p, scratch, s);
+    return;
   }
   const int nc = leaf3_width(p.nrhs, p.trsm != 0);
   auto go = [&](auto kern, int width, int smem) {

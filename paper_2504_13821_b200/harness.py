@@ -181,14 +181,14 @@ def _cublas_call(op, spec, n, m, A, B):
         f = lib.cmp_trsm
         f.argtypes = [i32, i32, i32, i32, i32, vp, i64, vp, i64, i64, i32]
         f.restype = ctypes.c_double
-        return lambda: f(dtype, side, uplo, trans, diag, A.data_ptr(), n, B.data_ptr(), rows, cols, 1)
+        return lambda: f(dtype, side, uplo, trans, diag, A.data_ptr(), n, B.data_ptr(), rows, cols, 0)
     out = torch.empty_like(B)
     f = lib.cmp_trmm
     f.argtypes = [i32, i32, i32, i32, i32, vp, i64, vp, vp, i64, i64, i32]
     f.restype = ctypes.c_double
 
     def run():
-        t = f(dtype, side, uplo, trans, diag, A.data_ptr(), n, B.data_ptr(), out.data_ptr(), rows, cols, 1)
+        t = f(dtype, side, uplo, trans, diag, A.data_ptr(), n, B.data_ptr(), out.data_ptr(), rows, cols, 0)
         B.copy_(out)
         return t
     return run

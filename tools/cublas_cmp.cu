@@ -13,12 +13,15 @@ cublasHandle_t handle() {
   if (!h) cublasCreate(&h);
   return h;
 }
+// reps <= 0: exactly one (timed) call, no warm-up -- for in-place solves whose
+// result is checked afterwards.
 template <typename F>
 double timed(F f, int reps) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  f();
+  if (reps > 0) f();
+  else reps = 1;
   cudaDeviceSynchronize();
   float best = 1e30f;
   for (int i = 0; i < reps; ++i) {
