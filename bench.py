@@ -659,6 +659,12 @@ def main():
         log(f"e2e: {e2e['value']:.1f} GFLOP/s")
         del Ah, Bh, Bh0
 
+    # End to end through the C++ drop-in with the reference caller's memory:
+    # std::vector-backed MatrixBuffers (pageable), tests/cpp/dropin_bench.cpp.
+    e2e_pageable = None
+    if not args.no_e2e and world == 1:
+        e2e_pageable = run_dropin_pageable(args, n, min(m, 65536))
+
     # cuBLAS reported comparison (same inputs, device-resident).
     cublas = None
     if not args.no_cublas and world == 1:
@@ -691,13 +697,39 @@ def main():
             "pct_of_peak": value / 1e3 / (peak64 * world) * 100,
             "residual": {"eta": eta, "finite": finite, "bound": 32,
                          "definition": "||tril(A) X - B||_max / (||A||_inf max(|X|,|B|,1) n eps), 8 sampled columns"},
-            "trmm": trmm, "fp32": fp32, "c5_strong": c5, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "trmm": trmm, "fp32": fp32, "c5_strong": c5, "e2e": e2e, "e2e_pageable": e2e_pageable,
+            "roofline": roofline, "cpu_baseline": cpu,
             "cublas": cublas,
             "clocks": clocks, "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def run_dropin_pageable(args, n, m):
+    """tests/cpp/dropin_bench: rectri::rec_trsm<double> on std::vector-backed
+    MatrixBuffers (pageable host memory, the reference caller's own), wall
+    clock per call with steady_clock; the library stages through pinned bounce
+    buffers with host threads overlapping the GPU (csrc/host_stage.h)."""
+    import subprocess
+
+    exe = ROOT / "tests" / "cpp" / "build" / "dropin_bench"
+    if not exe.exists():
+        return {"error": "tests/cpp/build/dropin_bench not built"}
+    steps = max(1, min(args.steps, 5))
+    try:
+        r = subprocess.run([str(exe), str(n), str(m), str(steps), "2"], capture_output=True, text=True, timeout=900)
+        d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)}
+    d.update({"value": float(n) * n * m / (d["ms_per_step"] * 1e-3) / 1e9, "unit": "GFLOP/s",
+              "h2d_bytes_per_step": ((n * n + n * args.threshold) // 2 + n * m) * 8,
+              "d2h_bytes_per_step": n * m * 8, "rc": r.returncode,
+              "path": "C++ drop-in rectri::rec_trsm<double>, std::vector MatrixBuffers (pageable); pinned bounce "
+                      "staging by host threads overlapping the streamed transfers; wall clock per call"})
+    log(f"e2e pageable: {d['value']:.1f} GFLOP/s ({d['ms_per_step']:.1f} ms/step, eta {d['eta']:.2e})")
+    return d
 
 
 def cublas_compare(A, B0, n, m, args):

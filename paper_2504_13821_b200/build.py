@@ -21,8 +21,8 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "lib" / "obj"
 LIB = PKG / "lib" / "librectri_cu.so"
 SOURCES = ["gemm_f64.cu", *[f"gemm_f64_cfg{i}.cu" for i in range(19)], "gemm_f64_tma.cu",
-           *[f"gemm_f64_tma_cfg{i}.cu" for i in range(7)], "gemm_f32.cu", "sgemm_tf32x3.cu", "leaf.cu", "leaf64.cu", "leaf64_v3.cu", "leaf64_v4.cu", "leaf32_v3.cu", "aux.cu",
-           "driver.cu", "bench_host.cpp"]
+           *[f"gemm_f64_tma_cfg{i}.cu" for i in range(7)], "gemm_f32.cu", "sgemm_tf32x3.cu", "leaf.cu", "leaf64.cu", "leaf64_v3.cu", "leaf64_v4.cu", "leaf64_v5.cu", "leaf32_v3.cu", "aux.cu",
+           "driver.cu", "host_stage.cpp", "bench_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
     "-O3",
@@ -120,8 +120,28 @@ def build_dropin_example() -> Path:
     return EXAMPLE_BIN
 
 
+BENCH_SRC = ROOT / "tests" / "cpp" / "dropin_bench.cpp"
+BENCH_BIN = ROOT / "tests" / "cpp" / "build" / "dropin_bench"
+
+
+def build_dropin_bench() -> Path:
+    """The reference-caller-shaped e2e timer (std::vector MatrixBuffers
+    through the C++ drop-in) that bench.py runs for its e2e_pageable line."""
+    BENCH_BIN.parent.mkdir(parents=True, exist_ok=True)
+    deps = [BENCH_SRC, LIB, ROOT / "include" / "rectri_b200.hpp", ROOT / "include" / "rectri_cu.h"]
+    if _stale(BENCH_BIN, deps):
+        cmd = [os.environ.get("CXX", "g++"), "-std=c++17", "-O2", "-Wall", "-pthread", f"-I{ROOT / 'include'}",
+               str(BENCH_SRC), f"-L{LIB.parent}", "-lrectri_cu",
+               "-Wl,-rpath,$ORIGIN/../../../paper_2504_13821_b200/lib", "-o", str(BENCH_BIN)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"drop-in bench failed to build:\n{r.stderr}")
+    return BENCH_BIN
+
+
 if __name__ == "__main__":
     build(verbose=True)
     build_dropin_example()
+    build_dropin_bench()
     build_cublas_cmp()
     sys.exit(0)

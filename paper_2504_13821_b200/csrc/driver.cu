@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../../include/rectri_cu.h"
+#include "host_stage.h"
 #include "launch.h"
 
 namespace rectri_cu {
@@ -602,6 +603,7 @@ struct GraphEntry {
     for (int k = 0; k < scratch.n; ++k) {
       if (scratch.leaf[k]) cudaFree(scratch.leaf[k]);
       if (scratch.split[k]) cudaFree(scratch.split[k]);
+      if (scratch.gemm_ws[k]) cudaFree(scratch.gemm_ws[k]);
     }
     if (packed) cudaFree(packed);
     if (leaf_meta) cudaFree(leaf_meta);
@@ -738,12 +740,8 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
       pbase.unit = spec.diag == RECTRI_CU_UNIT ? 1 : 0;
       pbase.trsm = op == kTrsm ? 1 : 0;
       pbase.alpha = static_cast<T>(eff.alpha);
-      // fp64 TRMM leaves of a stream panel this wide run the v4 kernel,
-      // which reads its triangles in ascending row order
-      const i64 rhs_all = spec.side == RECTRI_CU_LEFT ? B.cols : B.rows;
-      const int P0 = g_prof.on ? 1 : panel_streams(rhs_all);
-      const i64 w0 = P0 <= 1 ? rhs_all : ((rhs_all + P0 - 1) / P0 + 63) / 64 * 64;
-      pbase.pack_asc = std::is_same<T, double>::value && op == kTrmm && leaf4_use(w0) ? 1 : 0;
+      // fp64 TRMM leaves v4 / v5 read their triangles in ascending row order
+      pbase.pack_asc = std::is_same<T, double>::value && op == kTrmm && leaf_trmm_asc() ? 1 : 0;
     }
   }
   // Concurrent TRMM nodes (ConcCtx): packed leaves only (no per-stream leaf
@@ -799,10 +797,23 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
     const i64 h = A.rows - A.rows / 2;
     const i64 pw = P_ <= 1 ? rhs_ : ((rhs_ + P_ - 1) / P_ + 63) / 64 * 64;  // a stream's panel
     const size_t split_need = 2 * static_cast<size_t>(h * h + h * std::min(pw, rhs_));
+    // stream-K DGEMM workspace when the level-1 update has more 64x64 tiles
+    // than the resident slots (smaller updates never use it)
+    const int sk_ctas = std::is_same<T, double>::value ? gemm_sk_ctas() : 0;
+    const bool sk = sk_ctas > 0 && ((A.rows / 2 + 63) / 64) * ((std::min(pw, rhs_) + 63) / 64) > sk_ctas;
     CallScratch& cs = g->scratch;
-    for (int k = 0; k < P_ && (leaf_scratch || split); ++k) {
+    for (int k = 0; k < P_ && (leaf_scratch || split || sk); ++k) {
       cs.stream[k] = k == 0 ? s : res.aux[k - 1];
       cs.n = k + 1;
+      if (sk) {
+        const size_t bytes = gemm_sk_ws_bytes(sk_ctas);
+        cuda_check(cudaMalloc(&cs.gemm_ws[k], bytes), "stream-K workspace alloc");
+        int* fl = reinterpret_cast<int*>(cs.gemm_ws[k] + static_cast<size_t>(sk_ctas) * 4 * 32 * 32);
+        cuda_check(cudaMemsetAsync(fl, 0, static_cast<size_t>(sk_ctas) * sizeof(int), s), "workspace flags");
+        cuda_check(cudaStreamSynchronize(s), "workspace flags");
+        cs.gemm_ctas[k] = sk_ctas;
+        g->bytes += bytes;
+      }
       if (leaf_scratch) {
         cuda_check(cudaMalloc(&cs.leaf[k], leaf_scratch_bytes()), "leaf scratch alloc");
         g->bytes += leaf_scratch_bytes();
@@ -1144,7 +1155,8 @@ void run_host_panels(OpK op, const Spec& spec, DView<const T> dA, DView<T> hB, i
 // uses run_host_panels.
 template <typename T>
 bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, DView<T> hB, i64 threshold,
-                       const BackendInfo& be, rectri_cu_event_fn sink, void* user, int dev) {
+                       const BackendInfo& be, rectri_cu_event_fn sink, void* user, int dev,
+                       PageableStager* pg = nullptr) {
   const bool left = spec.side == RECTRI_CU_LEFT;
   const i64 n = A.rows, brows = hB.rows, bcols = hB.cols;
   const size_t bbytes = static_cast<size_t>(brows * bcols) * sizeof(T);
@@ -1249,6 +1261,14 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
   };
   auto copy2d = [&](T* dst, i64 dld, const T* src, i64 sld, i64 rows, i64 cols, cudaMemcpyKind kind,
                     cudaStream_t st) {
+    if (pg && kind == cudaMemcpyHostToDevice && pg->covers(src)) {  // pageable source: pinned bounce
+      pg->h2d(dst, sizeof(T) * dld, src, sizeof(T) * sld, sizeof(T) * rows, cols, st);
+      return;
+    }
+    if (pg && kind == cudaMemcpyDeviceToHost && pg->covers(dst)) {
+      pg->d2h(dst, sizeof(T) * dld, src, sizeof(T) * sld, sizeof(T) * rows, cols, st);
+      return;
+    }
     cuda_check(cudaMemcpy2DAsync(dst, sizeof(T) * dld, src, sizeof(T) * sld, sizeof(T) * rows, cols, kind, st),
                "staged copy");
   };
@@ -1293,14 +1313,8 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
       packs = static_cast<double*>(staging(*res, 2, leaves.size() * leaf3_scratch_doubles() * sizeof(double)));
     }
     std::vector<cudaEvent_t> packed_evs(units.size(), nullptr);
-    // TRMM triangles in the v4 leaf's ascending order when the first panel's
-    // stream parts are wide enough for it (the order is fixed for all panels)
-    int pack_asc = 0;
-    if (pack_once && op == kTrmm) {
-      const i64 prhs0 = std::min(rhs, tw);
-      const int P0 = panel_streams(prhs0);
-      pack_asc = leaf4_use(((prhs0 + P0 - 1) / P0 + 63) / 64 * 64) ? 1 : 0;
-    }
+    // TRMM triangles in the v4 / v5 leaves' ascending order
+    const int pack_asc = pack_once && op == kTrmm && leaf_trmm_asc() ? 1 : 0;
     for (int tp = 0; tp < TP && tp * tw < rhs; ++tp) {
       const i64 t0 = tp * tw, t1 = std::min(rhs, t0 + tw);
       // H2D in first-use order (A blocks in the first panel); ready[i] gates unit i.
@@ -1435,6 +1449,7 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
     cuda_check(cudaStreamSynchronize(ds), "synchronize");
     cuda_check(cudaStreamSynchronize(cs), "synchronize");
     cuda_check(cudaStreamSynchronize(hs), "synchronize");
+    if (pg) pg->finish();  // pageable B: the copy-backs into user memory
     if (trace) {
       fprintf(stderr, "e2e trace: host enqueue %.2f ms\n", host_ms);
       float t[3] = {0, 0, 0};
@@ -1534,9 +1549,21 @@ void rec_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
     run_device<T>(op, spec, dA, B, threshold, be2, sink, user, dev, true);
     return;
   }
+  // Pageable (e.g. std::vector-backed) host operands go through pinned
+  // bounce buffers with host-thread copies overlapping the GPU (host_stage.h);
+  // RECTRI_CU_PAGEABLE_DIRECT=1 copies straight from pageable memory instead.
+  std::unique_ptr<PageableStager> pg;
+  const bool a_pg = !a_dev && is_pageable_host(Av.origin), b_pg = is_pageable_host(Bv.origin);
+  if ((a_pg || b_pg) && !getenv("RECTRI_CU_PAGEABLE_DIRECT")) {
+    const size_t a_bytes = static_cast<size_t>((n - 1) * A.ld + n) * sizeof(T);
+    const size_t b_bytes = static_cast<size_t>((B.cols - 1) * B.ld + B.rows) * sizeof(T);
+    pg = std::make_unique<PageableStager>(dev, a_pg ? A.p : nullptr, a_pg ? a_bytes : 0, b_pg ? B.p : nullptr,
+                                          b_pg ? b_bytes : 0);
+  }
   if (!getenv("RECTRI_CU_HOST_PANEL") &&
-      run_host_streamed<T>(op, spec, A, a_dev, B, threshold, be2, sink, user, dev))
+      run_host_streamed<T>(op, spec, A, a_dev, B, threshold, be2, sink, user, dev, pg.get()))
     return;
+  pg.reset();
   cudaEvent_t a_ready = nullptr;
   if (!a_dev) {
     copy_triangle_h2d<T>(const_cast<T*>(dA.p), A, spec.uplo, res->h2d);
@@ -1835,6 +1862,7 @@ void rectri_cu_release_staging(void) {
     }
   }
   cudaSetDevice(prev);
+  release_pageable_bounce();
 }
 
 int64_t rectri_cu_device_bytes_held(void) {

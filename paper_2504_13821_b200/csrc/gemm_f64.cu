@@ -60,6 +60,7 @@ int choose_tma(const GemmParams<double>& p) {
 
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
+  if (launch_gemm_f64_sk(p, ta, tb, s)) return;  // mid-size tile counts: stream-K, same bits
   if (launch_gemm_f64_tma(p, ta, tb, s, choose_tma(p))) return;
   const bool vec2 = aligned16(p.A) && aligned16(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
   kRuns[choose(p)](p, ta, tb, vec2, s);

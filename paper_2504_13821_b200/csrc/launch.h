@@ -72,12 +72,19 @@ void launch_leaf3_pack_all(const LeafParams<double>& base, const long long* d_r0
 size_t leaf3_scratch_doubles();
 // Packs one leaf's triangle (p.A, p.n, variant flags) into dst.
 void launch_leaf3_pack(const LeafParams<double>& p, double* dst, cudaStream_t s);
+int leaf_version();  // RECTRI_CU_LEAF (fp64: 1 = leaf.cu, 2 = leaf64.cu, 3 = leaf64_v3.cu, 4 = v3/v4/v5 by shape)
 int leaf3_width(long long nrhs, bool trsm);  // fp64 leaf v3 panel width (8 / 16 / 32)
 // fp64 leaf v4 (leaf64_v4.cu): column-owning warps, bitwise the v3 arithmetic;
 // used (RECTRI_CU_LEAF >= 4, the default) for leaves with many right-hand sides.
 bool leaf4_use(long long nrhs);
 void launch_leaf_f64_v4(const LeafParams<double>& p, const double* packed, cudaStream_t s);
-int leaf_version();  // RECTRI_CU_LEAF (fp64: 1 = leaf.cu, 2 = leaf64.cu, 3 = leaf64_v3.cu)
+// fp64 TRMM leaf v5 (leaf64_v5.cu): row-block-owning warps for few
+// right-hand sides; width 0 = not used for this nrhs.
+int leaf5_width(long long nrhs);
+void launch_leaf_f64_v5_trmm(const LeafParams<double>& p, const double* packed, int width, cudaStream_t s);
+// fp64 TRMM triangles are packed in ascending row order (v4 / v5) rather than
+// v3's descending one: RECTRI_CU_LEAF >= 4.
+inline bool leaf_trmm_asc() { return leaf_version() >= 4; }
 // Allocates the v2 fp64 leaf's per-stream scratch (call before capturing on s).
 void leaf_scratch_reserve(cudaStream_t s);
 void launch_leaf_f32(const LeafParams<float>& p, cudaStream_t s);     // leaf64.cu dispatch
@@ -123,6 +130,8 @@ struct CallScratch {
   double* leaf[kMax] = {};
   float* split[kMax] = {};
   size_t split_floats[kMax] = {};
+  double* gemm_ws[kMax] = {};  // stream-K DGEMM partial tiles + flags (gemm_f64_sk.cuh)
+  int gemm_ctas[kMax] = {};
   int find(cudaStream_t s) const {
     for (int k = 0; k < n; ++k)
       if (stream[k] == s) return k;
@@ -132,5 +141,10 @@ struct CallScratch {
 void set_call_scratch(const CallScratch* cs);  // thread-local; nullptr to clear
 const CallScratch* call_scratch();
 size_t leaf_scratch_bytes();  // one stream's unpacked-leaf scratch
+// Stream-K fp64 GEMM (gemm_f64_sk.cuh): bitwise the data-parallel kernel;
+// used for mid-size tile counts when the stream has a workspace.
+bool launch_gemm_f64_sk(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s);
+int gemm_sk_ctas();                  // its persistent grid on the current device
+size_t gemm_sk_ws_bytes(int ctas);   // workspace bytes for that grid (flags zeroed before first use)
 
 }  // namespace rectri_cu

@@ -414,14 +414,21 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
   using namespace leaf64v3;
   const int nblk = (p.n + kRB - 1) / kRB;
   const bool zero = !p.trsm && p.alpha == 0.0;
-  // v4 (bitwise the same arithmetic) for many right-hand sides; a TRMM
-  // triangle packed in ascending order can only be consumed by v4.
-  const bool v4 = !zero && (prepacked ? (p.trsm ? leaf4_use(p.nrhs) : p.pack_asc != 0) : leaf4_use(p.nrhs));
+  // Bitwise-identical kernels by shape: TRSM v4 for many right-hand sides,
+  // else v3; TRMM (triangle in ascending order, RECTRI_CU_LEAF >= 4) v5 for
+  // few right-hand sides, else v4.
+  const bool asc = !p.trsm && (prepacked ? p.pack_asc != 0 : leaf_trmm_asc());
+  const int w5 = asc ? leaf5_width(p.nrhs) : 0;
+  const bool v4 = !zero && (p.trsm ? leaf4_use(p.nrhs) : asc && w5 == 0);
   if (!prepacked && !zero) {
     LeafParams<double> q = p;
-    q.pack_asc = v4 ? 1 : 0;
+    q.pack_asc = asc ? 1 : 0;
     pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(q, scratch);
     ++launch_counter();
+  }
+  if (!zero && w5 > 0) {
+    launch_leaf_f64_v5_trmm(p, scratch, w5, s);
+    return;
   }
   if (v4) {
     launch_leaf_f64_v4(p, scratch, s);

@@ -172,10 +172,11 @@ def test_default_leaf_replay_stress(cuda, monkeypatch, op, dtype, width):
 @pytest.mark.parametrize("side,uplo,trans,diag", VARIANTS)
 def test_leaf_v4_bitwise_equals_v3(cuda, monkeypatch, op, side, uplo, trans, diag):
     """v4 (leaf64_v4.cu: column-owning warps, pipelined panel, no CTA
-    barriers) performs v3's per-element arithmetic: identical bits on every
-    variant, ragged orders / right-hand-side counts, alpha, every v4 panel
-    configuration -- so choosing v4 or v3 by right-hand-side count never
-    changes a result (the RHS-sharding invariant)."""
+    barriers) and, for TRMM, v5 (leaf64_v5.cu: row-block-owning warps)
+    perform v3's per-element arithmetic: identical bits on every variant,
+    ragged orders / right-hand-side counts, alpha, every panel configuration
+    -- so choosing among them by right-hand-side count never changes a
+    result (the RHS-sharding invariant)."""
     rng = np.random.default_rng(500 + 8 * side + 4 * uplo + 2 * trans + diag)
     for n, m, alpha in ((1, 3, 1.0), (33, 70, 1.0), (100, 65, -0.75), (256, 200, 1.0), (255, 97, 2.5)):
         s = oracle.spec(side, uplo, trans, diag, alpha)
@@ -183,11 +184,20 @@ def test_leaf_v4_bitwise_equals_v3(cuda, monkeypatch, op, side, uplo, trans, dia
         monkeypatch.delenv("RECTRI_CU_LEAF4_MIN", raising=False)
         v3 = _base(op, s, a, b, 3, monkeypatch)
         monkeypatch.setenv("RECTRI_CU_LEAF4_MIN", "1")
+        monkeypatch.setenv("RECTRI_CU_LEAF5_MAX", "0")  # v4 for TRMM too
         for cfg in ("0", "1", "2", "3", "4"):
             monkeypatch.setenv("RECTRI_CU_LEAF4_CFG", cfg)
             v4 = _base(op, s, a, b, 4, monkeypatch)
             assert oracle.bitwise_equal(v3, v4), (op, side, uplo, trans, diag, n, m, alpha, cfg)
         check_against_oracle(op, s, a, b, v4)
+        if op == "trmm":  # v5: row-block-owning warps, every panel width
+            monkeypatch.setenv("RECTRI_CU_LEAF5_MAX", str(1 << 30))
+            for nc in ("8", "16", "32"):
+                monkeypatch.setenv("RECTRI_CU_LEAF5_NC", nc)
+                v5 = _base(op, s, a, b, 4, monkeypatch)
+                assert oracle.bitwise_equal(v3, v5), (op, side, uplo, trans, diag, n, m, alpha, "v5", nc)
+            monkeypatch.delenv("RECTRI_CU_LEAF5_NC")
+        monkeypatch.delenv("RECTRI_CU_LEAF5_MAX")
 
 
 @pytest.mark.parametrize("op", ["trsm", "trmm"])
