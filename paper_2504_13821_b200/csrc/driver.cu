@@ -9,6 +9,7 @@
 // captured once into a CUDA graph and replayed on later calls, with the
 // recorded event list replayed to the caller's sink.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -72,6 +73,20 @@ int guarded(F&& f, i64* index_out) {
     return RECTRI_CU_CUDA;
   }
 }
+
+// NVTX ranges (tracing): one per library call and per recursion
+// level of the host traversal (capture / descriptor runs / direct launches),
+// so nsys / ncu timelines group the kernels by call and level.  Header-only
+// NVTX v3: a no-op unless a tool injects itself.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  Nvtx(const char* fmt, long long a, long long b) {
+    char buf[96];
+    std::snprintf(buf, sizeof buf, fmt, a, b);
+    nvtxRangePushA(buf);
+  }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 // ---------------------------------------------------------------------------
 // Boundary types.
@@ -293,7 +308,7 @@ void enqueue_gemm(T alpha, bool ta, DView<const T> A, bool tb, DView<const T> B,
 // internal recursion with the same schema (no events: semantically one call).
 template <typename T>
 void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s,
-                  double* packed = nullptr, int pack_asc = 0);
+                  double* packed = nullptr, int pack_asc = 0, int direct = 0);
 
 // One kernel of the recursion, as emitted by a descriptor run (the streamed
 // host path executes these itself).
@@ -381,6 +396,10 @@ class Recursion {
       return;
     }
     const i64 mid = n / 2;  // split_half
+    // the upper levels only (each range formats a string on the host)
+    std::unique_ptr<Nvtx> range;
+    if (n >= 1024) range = std::make_unique<Nvtx>("rectri node n=%lld rhs=%lld", static_cast<long long>(n),
+                                                  static_cast<long long>(rhs));
     const Schema sc = schema_for(op_, spec.side, spec.uplo, spec.trans);
     const DView<const T> a11 = A.sub(0, 0, mid, mid);
     const DView<const T> a22 = A.sub(mid, mid, n - mid, n - mid);
@@ -485,7 +504,7 @@ LeafParams<T> leaf_params(OpK op, const Spec& spec, DView<const T> A, DView<T> B
 
 template <typename T>
 void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaStream_t s, double* packed,
-                  int pack_asc) {
+                  int pack_asc, int direct) {
   const i64 n = A.rows;
   const bool left = spec.side == RECTRI_CU_LEFT;
   const i64 rhs = left ? B.cols : B.rows;
@@ -511,6 +530,7 @@ void enqueue_base(OpK op, const Spec& spec, DView<const T> A, DView<T> B, cudaSt
   p.alpha = static_cast<T>(spec.alpha);
   p.packed = packed;
   p.pack_asc = pack_asc;
+  p.direct = direct;
   ProfScope prof(1, static_cast<double>(n) * n * rhs, s);
   K<T>::leaf(p, s);
 }
@@ -603,7 +623,6 @@ struct GraphEntry {
     for (int k = 0; k < scratch.n; ++k) {
       if (scratch.leaf[k]) cudaFree(scratch.leaf[k]);
       if (scratch.split[k]) cudaFree(scratch.split[k]);
-      if (scratch.gemm_ws[k]) cudaFree(scratch.gemm_ws[k]);
     }
     if (packed) cudaFree(packed);
     if (leaf_meta) cudaFree(leaf_meta);
@@ -797,23 +816,10 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
     const i64 h = A.rows - A.rows / 2;
     const i64 pw = P_ <= 1 ? rhs_ : ((rhs_ + P_ - 1) / P_ + 63) / 64 * 64;  // a stream's panel
     const size_t split_need = 2 * static_cast<size_t>(h * h + h * std::min(pw, rhs_));
-    // stream-K DGEMM workspace when the level-1 update has more 64x64 tiles
-    // than the resident slots (smaller updates never use it)
-    const int sk_ctas = std::is_same<T, double>::value ? gemm_sk_ctas() : 0;
-    const bool sk = sk_ctas > 0 && ((A.rows / 2 + 63) / 64) * ((std::min(pw, rhs_) + 63) / 64) > sk_ctas;
     CallScratch& cs = g->scratch;
-    for (int k = 0; k < P_ && (leaf_scratch || split || sk); ++k) {
+    for (int k = 0; k < P_ && (leaf_scratch || split); ++k) {
       cs.stream[k] = k == 0 ? s : res.aux[k - 1];
       cs.n = k + 1;
-      if (sk) {
-        const size_t bytes = gemm_sk_ws_bytes(sk_ctas);
-        cuda_check(cudaMalloc(&cs.gemm_ws[k], bytes), "stream-K workspace alloc");
-        int* fl = reinterpret_cast<int*>(cs.gemm_ws[k] + static_cast<size_t>(sk_ctas) * 4 * 32 * 32);
-        cuda_check(cudaMemsetAsync(fl, 0, static_cast<size_t>(sk_ctas) * sizeof(int), s), "workspace flags");
-        cuda_check(cudaStreamSynchronize(s), "workspace flags");
-        cs.gemm_ctas[k] = sk_ctas;
-        g->bytes += bytes;
-      }
       if (leaf_scratch) {
         cuda_check(cudaMalloc(&cs.leaf[k], leaf_scratch_bytes()), "leaf scratch alloc");
         g->bytes += leaf_scratch_bytes();
@@ -1513,6 +1519,9 @@ void rec_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
          side_name(spec.side));
   if (overlaps(Av, Bv)) fail(RECTRI_CU_ALIAS, "A and B views overlap");
   if (Av.rows == 0 || Bv.rows == 0 || Bv.cols == 0) return;
+  const Nvtx range(op == kTrsm ? "rectri rec_trsm n=%lld rhs=%lld" : "rectri rec_trmm n=%lld rhs=%lld",
+                   static_cast<long long>(Av.rows),
+                   static_cast<long long>(spec.side == RECTRI_CU_LEFT ? Bv.cols : Bv.rows));
 
   DeviceGuard guard(be.device);
   int dev = 0;
@@ -1653,7 +1662,7 @@ void base_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
   if (n == 0 || rhs == 0) return;
   Staged<const T> A(Av, s);
   Staged<T> B(Bv, s);
-  enqueue_base<T>(op, spec, A.view, B.view, s);
+  enqueue_base<T>(op, spec, A.view, B.view, s, nullptr, 0, /*direct=*/1);
   cuda_check(cudaGetLastError(), "leaf launch");
   B.copy_back(s);
   cuda_check(cudaStreamSynchronize(s), "synchronize");

@@ -33,16 +33,13 @@ int forced_config() {  // RECTRI_CU_GEMM64_CFG=<id> pins one configuration (tuni
 
 int choose(const GemmParams<double>& p) {
   const int f = forced_config();
-  // A 32-deep k-tile zero-pads a K tail that a 16-deep one would not (a
-  // -0.0 accumulator could turn +0.0), so BK=32 configurations are only
-  // eligible when K % 32 == 0, where both produce identical bits.
-  const bool bk32 = f == 2 || f == 3 || f == 7 || f == 8 || f == 9;
-  if (f >= 0 && f < kNumCfg && (p.K % 32 == 0 || !bk32)) return f;
+  if (f >= 0 && f < kNumCfg) return f;
   // 64x64 CTAs: 4 warps (3 CTAs per SM) for the large levels, 8 warps (2 per
   // SM) when K <= 512 where more resident warps hide the short mainloop's
-  // prologue/epilogue latency (profiles/r01_gemm_cfg_sweep.txt).  Both use
-  // 16-deep k-tiles: identical per-element arithmetic.
-  return p.K <= 512 ? 17 : 6;
+  // prologue/epilogue latency (profiles/r01_gemm_cfg_sweep.txt: round-1
+  // configurations 6 and 17; the other 17 swept shapes are no longer built).
+  // Both use 16-deep k-tiles: identical per-element arithmetic.
+  return p.K <= 512 ? 1 : 0;
 }
 
 }  // namespace
@@ -60,7 +57,6 @@ int choose_tma(const GemmParams<double>& p) {
 
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
-  if (launch_gemm_f64_sk(p, ta, tb, s)) return;  // mid-size tile counts: stream-K, same bits
   if (launch_gemm_f64_tma(p, ta, tb, s, choose_tma(p))) return;
   const bool vec2 = aligned16(p.A) && aligned16(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
   kRuns[choose(p)](p, ta, tb, vec2, s);

@@ -1,8 +1,8 @@
-// fp64 DMMA GEMM, configuration 1: CTA 128x128x16, warps 4x4, 4 stages.
+// fp64 DMMA GEMM (cp.async), configuration 1: CTA 64x64x16, warps 4x2, 4 stages.
 #include "gemm_f64_kernel.cuh"
 
 namespace rectri_cu {
 void dgemm_cfg1(const GemmParams<double>& p, bool ta, bool tb, bool vec2, cudaStream_t s) {
-  dgemm::Config<128, 128, 16, 4, 4, 4>::run(p, ta, tb, vec2, s);
+  dgemm::Config<64, 64, 16, 4, 2, 4>::run(p, ta, tb, vec2, s);
 }
 }  // namespace rectri_cu

@@ -344,26 +344,9 @@ struct Config {
 
 // Entry points of the instantiated configurations (gemm_f64_cfg*.cu).
 using DgemmRun = void (*)(const GemmParams<double>&, bool, bool, bool, cudaStream_t);
-#define RECTRI_DGEMM_CONFIGS(X)          \
-  X(0, 128, 128, 16, 2, 4, 4)            \
-  X(1, 128, 128, 16, 4, 4, 4)            \
-  X(2, 128, 128, 32, 2, 4, 3)            \
-  X(3, 128, 128, 32, 4, 4, 3)            \
-  X(4, 128, 64, 16, 4, 2, 4)             \
-  X(5, 64, 128, 16, 2, 4, 4)             \
-  X(6, 64, 64, 16, 2, 2, 4)              \
-  X(7, 64, 128, 32, 2, 4, 3)             \
-  X(8, 128, 64, 32, 4, 2, 3)             \
-  X(9, 64, 64, 32, 2, 2, 3)              \
-  X(10, 64, 64, 16, 1, 2, 4)             \
-  X(11, 64, 64, 16, 2, 2, 3)             \
-  X(12, 64, 128, 16, 2, 2, 4)            \
-  X(13, 128, 64, 16, 2, 2, 4)            \
-  X(14, 64, 64, 16, 2, 1, 4)             \
-  X(15, 64, 64, 16, 2, 2, 4)             \
-  X(16, 64, 64, 16, 2, 2, 4)             \
-  X(17, 64, 64, 16, 4, 2, 4)             \
-  X(18, 64, 64, 16, 2, 4, 4)
+#define RECTRI_DGEMM_CONFIGS(X) \
+  X(0, 64, 64, 16, 2, 2, 4)     \
+  X(1, 64, 64, 16, 4, 2, 4)
 #define RECTRI_DECL(ID, BM, BN, BK, WM, WN, ST) \
   void dgemm_cfg##ID(const GemmParams<double>&, bool, bool, bool, cudaStream_t);
 RECTRI_DGEMM_CONFIGS(RECTRI_DECL)

@@ -48,7 +48,8 @@ struct LeafParams {
   int debug_skip = 0;
   long long* trace = nullptr;  // RECTRI_CU_LEAF_TRACE: per-CTA clock64 stamps (leaf64.cu)
   double* packed = nullptr;    // v3: this leaf's triangle already packed here (pack3_all_kernel)
-  int pack_asc = 0;            // packed TRMM blocks in ascending row order (the v4 leaf's; TRSM always is)
+  int pack_asc = 0;            // packed TRMM blocks in ascending row order (the v5 leaf's; TRSM always is)
+  int direct = 0;              // a direct trmm_base / trsm_base call (not inside a recursion)
 };
 
 constexpr int kLeafMax = 256;
@@ -72,17 +73,15 @@ void launch_leaf3_pack_all(const LeafParams<double>& base, const long long* d_r0
 size_t leaf3_scratch_doubles();
 // Packs one leaf's triangle (p.A, p.n, variant flags) into dst.
 void launch_leaf3_pack(const LeafParams<double>& p, double* dst, cudaStream_t s);
-int leaf_version();  // RECTRI_CU_LEAF (fp64: 1 = leaf.cu, 2 = leaf64.cu, 3 = leaf64_v3.cu, 4 = v3/v4/v5 by shape)
+int leaf_version();  // RECTRI_CU_LEAF (fp64: 1 = leaf.cu, 2 = leaf64.cu, 3 = leaf64_v3.cu, 4 = v3 + v5 TRMM)
 int leaf3_width(long long nrhs, bool trsm);  // fp64 leaf v3 panel width (8 / 16 / 32)
-// fp64 leaf v4 (leaf64_v4.cu): column-owning warps, bitwise the v3 arithmetic;
-// used (RECTRI_CU_LEAF >= 4, the default) for leaves with many right-hand sides.
-bool leaf4_use(long long nrhs);
-void launch_leaf_f64_v4(const LeafParams<double>& p, const double* packed, cudaStream_t s);
 // fp64 TRMM leaf v5 (leaf64_v5.cu): row-block-owning warps for few
-// right-hand sides; width 0 = not used for this nrhs.
+// right-hand sides, bitwise the v3 arithmetic; width 0 = not used for nrhs.
+// Direct trmm_base calls use it; inside the recursion it is opt-in
+// (RECTRI_CU_LEAF=4), since beside the other stream's GEMMs v3 measured faster.
 int leaf5_width(long long nrhs);
 void launch_leaf_f64_v5_trmm(const LeafParams<double>& p, const double* packed, int width, cudaStream_t s);
-// fp64 TRMM triangles are packed in ascending row order (v4 / v5) rather than
+// Recursion TRMM triangles are packed in v5's ascending row order rather than
 // v3's descending one: RECTRI_CU_LEAF >= 4.
 inline bool leaf_trmm_asc() { return leaf_version() >= 4; }
 // Allocates the v2 fp64 leaf's per-stream scratch (call before capturing on s).
@@ -130,8 +129,6 @@ struct CallScratch {
   double* leaf[kMax] = {};
   float* split[kMax] = {};
   size_t split_floats[kMax] = {};
-  double* gemm_ws[kMax] = {};  // stream-K DGEMM partial tiles + flags (gemm_f64_sk.cuh)
-  int gemm_ctas[kMax] = {};
   int find(cudaStream_t s) const {
     for (int k = 0; k < n; ++k)
       if (stream[k] == s) return k;
@@ -141,10 +138,5 @@ struct CallScratch {
 void set_call_scratch(const CallScratch* cs);  // thread-local; nullptr to clear
 const CallScratch* call_scratch();
 size_t leaf_scratch_bytes();  // one stream's unpacked-leaf scratch
-// Stream-K fp64 GEMM (gemm_f64_sk.cuh): bitwise the data-parallel kernel;
-// used for mid-size tile counts when the stream has a workspace.
-bool launch_gemm_f64_sk(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s);
-int gemm_sk_ctas();                  // its persistent grid on the current device
-size_t gemm_sk_ws_bytes(int ctas);   // workspace bytes for that grid (flags zeroed before first use)
 
 }  // namespace rectri_cu

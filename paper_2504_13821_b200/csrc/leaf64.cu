@@ -454,13 +454,13 @@ double* scratch_for(cudaStream_t s, bool may_alloc) {
 }
 
 int leaf_version_env() {
-  // 4 (default): explicit-inverse diagonal blocks as DMMA products, v4
-  // (leaf64_v4.cu, column-owning warps) for leaves with many right-hand
-  // sides and v3 (leaf64_v3.cu) for the others -- bitwise the same; 3: v3
-  // only; 2: warp-shuffle substitution in the reference's order, bitwise
+  // 3 (default): explicit-inverse diagonal blocks as DMMA products
+  // (leaf64_v3.cu); 4: the same, with v5 (leaf64_v5.cu, row-block-owning
+  // warps, bitwise the same) for recursion TRMM leaves with few right-hand
+  // sides; 2: warp-shuffle substitution in the reference's order, bitwise
   // equal to v1 (leaf.cu).
   const char* e = getenv("RECTRI_CU_LEAF");
-  return e ? atoi(e) : 4;
+  return e ? atoi(e) : 3;
 }
 
 }  // namespace leaf64

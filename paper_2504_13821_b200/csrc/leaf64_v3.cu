@@ -414,24 +414,19 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
   using namespace leaf64v3;
   const int nblk = (p.n + kRB - 1) / kRB;
   const bool zero = !p.trsm && p.alpha == 0.0;
-  // Bitwise-identical kernels by shape: TRSM v4 for many right-hand sides,
-  // else v3; TRMM (triangle in ascending order, RECTRI_CU_LEAF >= 4) v5 for
-  // few right-hand sides, else v4.
-  const bool asc = !p.trsm && (prepacked ? p.pack_asc != 0 : leaf_trmm_asc());
-  const int w5 = asc ? leaf5_width(p.nrhs) : 0;
-  const bool v4 = !zero && (p.trsm ? leaf4_use(p.nrhs) : asc && w5 == 0);
+  // TRMM with few right-hand sides: v5 (bitwise the same arithmetic, its
+  // triangle in ascending row order) for direct base calls, and inside the
+  // recursion with RECTRI_CU_LEAF >= 4 (whose packed triangles are ascending).
+  const int w5 = p.trsm || zero ? 0 : leaf5_width(p.nrhs);
+  const bool v5 = w5 > 0 && (prepacked ? p.pack_asc != 0 : (p.direct || leaf_trmm_asc()));
   if (!prepacked && !zero) {
     LeafParams<double> q = p;
-    q.pack_asc = asc ? 1 : 0;
+    q.pack_asc = v5 ? 1 : 0;
     pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(q, scratch);
     ++launch_counter();
   }
-  if (!zero && w5 > 0) {
+  if (v5) {
     launch_leaf_f64_v5_trmm(p, scratch, w5, s);
-    return;
-  }
-  if (v4) {
-    launch_leaf_f64_v4(p, scratch, s);
     return;
   }
   const int nc = leaf3_width(p.nrhs, p.trsm != 0);

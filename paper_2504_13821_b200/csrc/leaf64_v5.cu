@@ -8,14 +8,20 @@
 // leaf need not run its 8 row blocks one after the other: compute warp w
 // owns the row blocks {w, nblk-1-w} of all NC columns, and the longest chain
 // of a CTA is nblk + 1 packed blocks instead of the nblk (nblk + 1) / 2 of
-// v3 / v4 (TRMM n = 256: 9 blocks instead of 36).  That is what matters
+// v3 (TRMM n = 256: 9 blocks instead of 36).  That is what matters
 // when the leaf has few right-hand sides (a 256 x 2048 leaf fills 128 CTAs)
 // and the GPU waits on the chain rather than on the tensor pipe.
 //
 // Arithmetic: per element exactly v3's (leaf64_v3.cu) -- J ascending with the
 // diagonal block L'_II last, DMMA.8x8x4 k-steps alternating between two
-// partial sums, X = alpha * (c0 + c1) -- so v5, v4 and v3 agree bit for bit
-// and the launcher may pick any of them by right-hand-side count.
+// partial sums, X = alpha * (c0 + c1) -- so v5 and v3 agree bit for bit and
+// the launcher may pick either by right-hand-side count.
+//
+// Where it is used: direct trmm_base calls (a 256 x 2048 leaf: 13.6 us vs
+// v3's 26 us, ncu); inside the recursion only with RECTRI_CU_LEAF=4, because
+// there the leaf runs beside the other right-hand-side stream's GEMMs and
+// v3's smaller shared-memory footprint measured faster (fp64 TRMM n = 4096:
+// 2202 us v3, 2226-2248 us v5; profiles/r02_leaf_v5.txt).
 //
 // Blocks stream from the packed triangle (pack3_kernel, ascending row order:
 // row I's blocks are contiguous) through a ring of STEPS: step s holds, for
@@ -246,7 +252,6 @@ void go(const LeafParams<double>& p, const double* P, cudaStream_t s) {
 // (RECTRI_CU_LEAF5_NC forces 8 / 16 / 32; RECTRI_CU_LEAF5_MAX: the largest
 // nrhs it is used for, default 4096).
 int leaf5_width(long long nrhs) {
-  if (leaf_version() < 4) return 0;
   const char* mx = getenv("RECTRI_CU_LEAF5_MAX");
   const long long maxr = mx ? atoll(mx) : 4096;
   if (nrhs > maxr) return 0;

@@ -168,63 +168,54 @@ def test_default_leaf_replay_stress(cuda, monkeypatch, op, dtype, width):
     rc.clear_graph_cache()
 
 
-@pytest.mark.parametrize("op", ["trsm", "trmm"])
 @pytest.mark.parametrize("side,uplo,trans,diag", VARIANTS)
-def test_leaf_v4_bitwise_equals_v3(cuda, monkeypatch, op, side, uplo, trans, diag):
-    """v4 (leaf64_v4.cu: column-owning warps, pipelined panel, no CTA
-    barriers) and, for TRMM, v5 (leaf64_v5.cu: row-block-owning warps)
-    perform v3's per-element arithmetic: identical bits on every variant,
-    ragged orders / right-hand-side counts, alpha, every panel configuration
-    -- so choosing among them by right-hand-side count never changes a
-    result (the RHS-sharding invariant)."""
+def test_leaf_v5_trmm_bitwise_equals_v3(cuda, monkeypatch, side, uplo, trans, diag):
+    """v5 (leaf64_v5.cu: row-block-owning warps, the TRMM leaf of direct
+    trmm_base calls) performs v3's per-element arithmetic: identical bits on
+    every variant, ragged orders / right-hand-side counts, alpha and every
+    panel width -- so choosing between them by right-hand-side count never
+    changes a result (the RHS-sharding invariant)."""
     rng = np.random.default_rng(500 + 8 * side + 4 * uplo + 2 * trans + diag)
-    for n, m, alpha in ((1, 3, 1.0), (33, 70, 1.0), (100, 65, -0.75), (256, 200, 1.0), (255, 97, 2.5)):
+    for n, m, alpha in ((1, 3, 1.0), (33, 70, 1.0), (100, 65, -0.75), (256, 200, 1.0), (255, 97, 2.5),
+                        (256, 5000, 1.0)):
         s = oracle.spec(side, uplo, trans, diag, alpha)
-        a, b = _inputs(op, s, n, m, rng)
-        monkeypatch.delenv("RECTRI_CU_LEAF4_MIN", raising=False)
-        v3 = _base(op, s, a, b, 3, monkeypatch)
-        monkeypatch.setenv("RECTRI_CU_LEAF4_MIN", "1")
-        monkeypatch.setenv("RECTRI_CU_LEAF5_MAX", "0")  # v4 for TRMM too
-        for cfg in ("0", "1", "2", "3", "4"):
-            monkeypatch.setenv("RECTRI_CU_LEAF4_CFG", cfg)
-            v4 = _base(op, s, a, b, 4, monkeypatch)
-            assert oracle.bitwise_equal(v3, v4), (op, side, uplo, trans, diag, n, m, alpha, cfg)
-        check_against_oracle(op, s, a, b, v4)
-        if op == "trmm":  # v5: row-block-owning warps, every panel width
-            monkeypatch.setenv("RECTRI_CU_LEAF5_MAX", str(1 << 30))
-            for nc in ("8", "16", "32"):
-                monkeypatch.setenv("RECTRI_CU_LEAF5_NC", nc)
-                v5 = _base(op, s, a, b, 4, monkeypatch)
-                assert oracle.bitwise_equal(v3, v5), (op, side, uplo, trans, diag, n, m, alpha, "v5", nc)
-            monkeypatch.delenv("RECTRI_CU_LEAF5_NC")
+        a, b = _inputs("trmm", s, n, m, rng)
+        monkeypatch.setenv("RECTRI_CU_LEAF5_MAX", "0")  # v3
+        v3 = _base("trmm", s, a, b, 3, monkeypatch)
+        monkeypatch.setenv("RECTRI_CU_LEAF5_MAX", str(1 << 30))
+        for nc in ("8", "16", "32"):
+            monkeypatch.setenv("RECTRI_CU_LEAF5_NC", nc)
+            v5 = _base("trmm", s, a, b, 3, monkeypatch)
+            assert oracle.bitwise_equal(v3, v5), (side, uplo, trans, diag, n, m, alpha, nc)
+        monkeypatch.delenv("RECTRI_CU_LEAF5_NC")
         monkeypatch.delenv("RECTRI_CU_LEAF5_MAX")
+        check_against_oracle("trmm", s, a, b, v5)
 
 
-@pytest.mark.parametrize("op", ["trsm", "trmm"])
 @pytest.mark.parametrize("side", [0, 1])
-def test_leaf_v4_in_recursion_bitwise(cuda, monkeypatch, op, side):
-    """The captured recursion with its triangles packed once (TRMM: in v4's
-    ascending order) gives identical bits with v4 leaves (default for wide
-    stream panels) and v3 leaves, device- and host-resident."""
+def test_leaf_v5_in_recursion_bitwise(cuda, monkeypatch, side):
+    """RECTRI_CU_LEAF=4 packs the recursion's TRMM triangles in v5's
+    ascending order and runs v5 leaves: identical bits to the default (v3),
+    device- and host-resident."""
     import paper_2504_13821_b200 as rc
+    import torch
 
     rng = np.random.default_rng(77 + side)
     n, m = 1024, 5000
     s = oracle.spec(side, 1, 0, 0, 1.0)
-    a, b = _inputs(op, s, n, m, rng)
-    fn = rec_trmm if op == "trmm" else rec_trsm
+    a, b = _inputs("trmm", s, n, m, rng)
     outs = []
     for version in ("3", "4"):
         monkeypatch.setenv("RECTRI_CU_LEAF", version)
         rc.clear_graph_cache()
         A, B = to_dev(a), to_dev(b)
-        fn(tspec(s), A.cview(), B.view(), Threshold(256), Backend.cuda())
+        rec_trmm(tspec(s), A.cview(), B.view(), Threshold(256), Backend.cuda())
         outs.append(to_np(B))
-        Bh = rc.MatrixBuffer.from_tensor(__import__("torch").from_numpy(np.ascontiguousarray(b)), device="cpu")
-        Ah = rc.MatrixBuffer.from_tensor(__import__("torch").from_numpy(np.ascontiguousarray(a)), device="cpu")
-        fn(tspec(s), Ah.cview(), Bh.view(), Threshold(256), Backend.cuda())
+        Ah = rc.MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(a)), device="cpu")
+        Bh = rc.MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(b)), device="cpu")
+        rec_trmm(tspec(s), Ah.cview(), Bh.view(), Threshold(256), Backend.cuda())
         outs.append(np.asfortranarray(Bh.numpy()))
     for o in outs[1:]:
         assert oracle.bitwise_equal(outs[0], o)
-    check_against_oracle(op, s, a, b, outs[0])
+    check_against_oracle("trmm", s, a, b, outs[0])
     rc.clear_graph_cache()
