@@ -21,7 +21,7 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "lib" / "obj"
 LIB = PKG / "lib" / "librectri_cu.so"
 SOURCES = ["gemm_f64.cu", *[f"gemm_f64_cfg{i}.cu" for i in range(2)], "gemm_f64_tma.cu",
-           *[f"gemm_f64_tma_cfg{i}.cu" for i in range(3)], "gemm_f32.cu", "sgemm_tf32x3.cu", "leaf.cu", "leaf64.cu", "leaf64_v3.cu", "leaf64_v5.cu", "leaf32_v3.cu", "aux.cu",
+           *[f"gemm_f64_tma_cfg{i}.cu" for i in range(4)], "gemm_f32.cu", "sgemm_tf32x3.cu", "leaf.cu", "leaf64.cu", "leaf64_v3.cu", "leaf64_v5.cu", "leaf32_v3.cu", "aux.cu",
            "driver.cu", "host_stage.cpp", "bench_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [

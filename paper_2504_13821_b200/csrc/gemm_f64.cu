@@ -49,10 +49,17 @@ int choose(const GemmParams<double>& p) {
 // TMA config 1 (64x64 CTAs, producer warp, 4 stages) reaches 36.1-36.4 TF/s
 // (97-98 % of the DMMA peak) from K = 8192 down to K = 1024 and, with the
 // batched epilogue, also beats the cp.async kernels at K = 512 (29.0 vs 27.5)
-// and K = 256 (19.8 vs 19.3) (profiles/r01_tma_gemm_sweep.txt).
+// and K = 256 (19.8 vs 19.3) (profiles/r01_tma_gemm_sweep.txt).  Updates with
+// fewer 64x64 tiles than 2 per SM are latency chains on a partly idle GPU:
+// config 3 (32x32 CTAs) gives them four times the CTAs
+// (RECTRI_CU_GEMM64_SMALL_TILES: that threshold in 64x64 tiles, 0 = off).
 int choose_tma(const GemmParams<double>& p) {
-  (void)p;
-  return 1;
+  static const long long small = [] {
+    const char* e = getenv("RECTRI_CU_GEMM64_SMALL_TILES");
+    return e ? atoll(e) : 296LL;
+  }();
+  const long long tiles64 = ceil_div(p.M, 64) * ceil_div(p.N, 64);
+  return tiles64 < small ? 3 : 1;
 }
 
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s) {

@@ -41,7 +41,8 @@ using DgemmTmaRun = bool (*)(const GemmParams<double>&, bool, bool, cudaStream_t
 #define RECTRI_DGEMM_TMA_CONFIGS(X) \
   X(0, 64, 64, 2, 2, 4, false)      \
   X(1, 64, 64, 2, 2, 4, true)       \
-  X(2, 64, 64, 2, 2, 6, true)
+  X(2, 64, 64, 2, 2, 6, true)       \
+  X(3, 32, 32, 2, 2, 4, true)
 #define RECTRI_DECL(ID, BM, BN, WM, WN, ST, PR) \
   bool dgemm_tma_cfg##ID(const GemmParams<double>&, bool, bool, cudaStream_t);
 RECTRI_DGEMM_TMA_CONFIGS(RECTRI_DECL)

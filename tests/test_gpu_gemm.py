@@ -131,7 +131,7 @@ def test_tma_kernel_bitwise_equals_cp_async(cuda, ta, tb, monkeypatch):
         av = A.cview().subview(2, 2, K, M) if ta else A.cview().subview(2, 2, M, K)
         bv = B.cview().subview(2, 2, N, K) if tb else B.cview().subview(2, 2, K, N)
         outs = []
-        for cfg in ("0", "1", "2", "3"):
+        for cfg in ("0", "1", "2", "3", "4"):
             monkeypatch.setenv("RECTRI_CU_GEMM64_TMA", cfg)
             C = to_dev(c0)
             gemm(-1.0, Trans(ta), av, Trans(tb), bv, 1.0, C.view().subview(2, 0, M, N))
