@@ -288,7 +288,7 @@ struct ProfScope {
 // validation): alpha == 0 or K == 0 only applies beta.
 template <typename T>
 void enqueue_gemm(T alpha, bool ta, DView<const T> A, bool tb, DView<const T> B, T beta,
-                  DView<T> C, cudaStream_t s) {
+                  DView<T> C, cudaStream_t s, int busy_gpu = 0) {
   const i64 M = C.rows, N = C.cols, Kd = ta ? A.rows : A.cols;
   if (M == 0 || N == 0) return;
   if (alpha == T(0) || Kd == 0) {  // apply_beta (gemm.cpp:129-142)
@@ -298,7 +298,7 @@ void enqueue_gemm(T alpha, bool ta, DView<const T> A, bool tb, DView<const T> B,
       K<T>::scale(C.p, C.ld, M, N, beta, s);
     return;
   }
-  GemmParams<T> p{M, N, Kd, alpha, beta, A.p, A.ld, B.p, B.ld, C.p, C.ld};
+  GemmParams<T> p{M, N, Kd, alpha, beta, A.p, A.ld, B.p, B.ld, C.p, C.ld, busy_gpu};
   ProfScope prof(0, 2.0 * static_cast<double>(M) * N * Kd, s);
   K<T>::gemm(p, ta, tb, s);
 }
@@ -426,15 +426,18 @@ class Recursion {
       kernels(KDesc<T>{false, spec, off, sc.read_b2 ? b2 : b1, dst, coeff, sc.off_trans != 0, sc.off_on_left});
     } else if (dry_) {
     } else if (sc.off_on_left)
-      enqueue_gemm<T>(coeff, sc.off_trans != 0, off, false, src, T(1), dst, s_);
+      enqueue_gemm<T>(coeff, sc.off_trans != 0, off, false, src, T(1), dst, s_, busy());
     else
-      enqueue_gemm<T>(coeff, false, src, sc.off_trans != 0, off, T(1), dst, s_);
+      enqueue_gemm<T>(coeff, false, src, sc.off_trans != 0, off, T(1), dst, s_, busy());
 
     if (sc.first_a22) run(spec, a11, b1, row0);
     else run(spec, a22, b2, row0 + mid);
   }
 
  private:
+  // TRMM calls with concurrent halves keep every GEMM on the large tiles (the
+  // other half fills the GPU beside them); a TRSM is a serial chain.
+  int busy() const { return conc != nullptr ? 1 : 0; }
   bool conc_node(const Schema& sc, i64 mid, i64 rhs, DView<T> dst) {
     if (!conc || dry_ || kernels || op_ != kTrmm || mid * rhs > conc->max_elems) return false;
     if (sc.first_a22 != sc.write_b2) return false;  // first half must be the GEMM's destination
@@ -457,9 +460,9 @@ class Recursion {
     emit(RECTRI_CU_EV_GEMM, dst.rows, dst.cols);
     if (before) before(false, off, sc.read_b2 ? b2 : b1, dst);
     if (sc.off_on_left)
-      enqueue_gemm<T>(T(1), sc.off_trans != 0, off, false, src, T(0), S, s2);
+      enqueue_gemm<T>(T(1), sc.off_trans != 0, off, false, src, T(0), S, s2, 1);
     else
-      enqueue_gemm<T>(T(1), false, src, sc.off_trans != 0, off, T(0), S, s2);
+      enqueue_gemm<T>(T(1), false, src, sc.off_trans != 0, off, T(0), S, s2, 1);
     cudaStream_t s1 = s_;
     s_ = s2;
     if (sc.first_a22) run(spec, a11, b1, row0);

@@ -50,16 +50,19 @@ int choose(const GemmParams<double>& p) {
 // (97-98 % of the DMMA peak) from K = 8192 down to K = 1024 and, with the
 // batched epilogue, also beats the cp.async kernels at K = 512 (29.0 vs 27.5)
 // and K = 256 (19.8 vs 19.3) (profiles/r01_tma_gemm_sweep.txt).  Updates with
-// fewer 64x64 tiles than 2 per SM are latency chains on a partly idle GPU:
-// config 3 (32x32 CTAs) gives them four times the CTAs
+// fewer than ~4 64x64 tiles per SM are latency chains on a partly idle GPU:
+// config 3 (32x32 CTAs) gives them four times the CTAs (fp64 TRSM n = m =
+// 1024: 107.8 -> 93.3 us, n = 2048: 406.7 -> 383.5 us; profiles/r02_small_tiles.txt)
 // (RECTRI_CU_GEMM64_SMALL_TILES: that threshold in 64x64 tiles, 0 = off).
+// Inside a TRMM with concurrent halves (p.busy_gpu) the other half fills the
+// GPU and the large tiles measured faster (n = 2048: 322.6 vs 327.4 us).
 int choose_tma(const GemmParams<double>& p) {
   static const long long small = [] {
     const char* e = getenv("RECTRI_CU_GEMM64_SMALL_TILES");
-    return e ? atoll(e) : 296LL;
+    return e ? atoll(e) : 600LL;
   }();
   const long long tiles64 = ceil_div(p.M, 64) * ceil_div(p.N, 64);
-  return tiles64 < small ? 3 : 1;
+  return !p.busy_gpu && tiles64 < small ? 3 : 1;
 }
 
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s) {

@@ -22,6 +22,9 @@ struct GemmParams {
   i64 ldb;
   T* C;
   i64 ldc;
+  // Scheduling hint (never changes a bit): 1 when other work runs beside this
+  // update (TRMM's concurrent halves), so it keeps the large tiles.
+  int busy_gpu = 0;
 };
 
 // Leaf (base-kernel) problem in the reference's Left form on a virtual lower

@@ -83,15 +83,16 @@ __device__ void pack32_block(const LeafParams<float>& p, float* __restrict__ P, 
     }
     return;
   }
-  if (tid < kRB) {  // -inv(L), column j = tid, in fp64
+  if (tid < kRB) {  // -inv(L), column j = tid, in fp64 (column-oriented: leaf64_v3.cu)
     const int j = tid;
     double y[kRB];
 #pragma unroll
-    for (int r = 0; r < kRB; ++r) {
-      double s = r == j ? 1.0 : 0.0;
+    for (int r = 0; r < kRB; ++r) y[r] = r == j ? 1.0 : 0.0;
 #pragma unroll
-      for (int q = 0; q < r; ++q) s = fma(-L[r][q], y[q], s);
-      y[r] = r < j ? 0.0 : s / L[r][r];
+    for (int q = 0; q < kRB; ++q) {
+      y[q] = q < j ? 0.0 : y[q] / L[q][q];
+#pragma unroll
+      for (int r = q + 1; r < kRB; ++r) y[r] = fma(-L[r][q], y[q], y[r]);
     }
 #pragma unroll
     for (int r = 0; r < kRB; ++r) dst[j * kRB + r] = static_cast<float>(-y[r]);  // [k = j][r]

@@ -112,16 +112,22 @@ __device__ void pack3_block(const LeafParams<double>& p, double* __restrict__ P,
     return;
   }
   // -inv(L): thread j solves L y = e_j by forward substitution
-  // (base_kernels.cpp:73-88 order: y_r = (e_r - sum_{p<r} L(r,p) y_p) / d_r).
+  // (base_kernels.cpp:73-88 order: y_r = (e_r - sum_{p<r} L(r,p) y_p) / d_r),
+  // written column-oriented: once y_p is known, every later row's running sum
+  // takes its term at once.  Each row still sums its terms in p order, so the
+  // values are those of the row-oriented loop; the 31 updates after each
+  // division are independent instead of one 496-long dependent chain (the
+  // packing kernel sits at the head of every small TRSM call).
   if (tid < kRB) {
     const int j = tid;
     double y[kRB];
 #pragma unroll
-    for (int r = 0; r < kRB; ++r) {
-      double s = r == j ? 1.0 : 0.0;
+    for (int r = 0; r < kRB; ++r) y[r] = r == j ? 1.0 : 0.0;  // running sums
 #pragma unroll
-      for (int q = 0; q < r; ++q) s = fma(-L[r][q], y[q], s);
-      y[r] = r < j ? 0.0 : s / L[r][r];
+    for (int q = 0; q < kRB; ++q) {
+      y[q] = q < j ? 0.0 : y[q] / L[q][q];
+#pragma unroll
+      for (int r = q + 1; r < kRB; ++r) y[r] = fma(-L[r][q], y[q], y[r]);
     }
 #pragma unroll
     for (int r = 0; r < kRB; ++r) dst[frag_pos(r, j)] = -y[r];

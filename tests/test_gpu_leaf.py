@@ -219,3 +219,4 @@ def test_leaf_v5_in_recursion_bitwise(cuda, monkeypatch, side):
         assert oracle.bitwise_equal(outs[0], o)
     check_against_oracle("trmm", s, a, b, outs[0])
     rc.clear_graph_cache()
+
