@@ -136,14 +136,13 @@ def setup_dist(args):
             nccl_log = None
             if "NCCL_DEBUG" not in os.environ:  # communicator INIT lines, echoed to stderr below
                 nccl_log = f"/tmp/rectri_bench_nccl.{os.getpid()}.log"
-                os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT", NCCL_DEBUG_FILE=nccl_log)
+                os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,ENV", NCCL_DEBUG_FILE=nccl_log)
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             dist.barrier()
             if nccl_log and os.path.exists(nccl_log):
-                for ln in Path(nccl_log).read_text().splitlines():
-                    if "nRanks" in ln or "Init COMPLETE" in ln or "NCCL version" in ln:
-                        log("nccl: " + ln.strip())
+                for ln in Path(nccl_log).read_text().splitlines()[:60]:
+                    log("nccl: " + ln.strip())
         log(f"bench: rank {dist.get_rank()} of {dist.get_world_size()} ({dist.get_backend()}), local rank {local}")
         if args.gpus != world:
             log(f"bench: note --gpus {args.gpus} but WORLD_SIZE {world}; the launcher's world size is used")

@@ -153,6 +153,12 @@ __global__ void __launch_bounds__(256) pack3_all_kernel(const LeafParams<double>
 }
 
 constexpr int kRing = 5;  // packed blocks in flight (bulk copies)
+// Independent DMMA accumulation chains per output tile: k-step kk of every
+// block goes to partial sum kk % kParts, the sums are added once per row
+// block.  (Four chains measured the same as two, TRSM n = m = 1024: 14.0 us
+// per leaf either way -- the dependency chain is not what bounds the small
+// leaves.)  v5 (leaf64_v5.cu) follows the same order.
+constexpr int kParts = 2;
 template <int NC>
 constexpr int smem_bytes() { return (kLeafMax * NC + kRB * NC + kRing * kBlk) * 8 + 2 * kRing * 8; }
 
@@ -292,11 +298,16 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
   auto ccol = [&](int e, int h) { return 8 * (nt0 + e) + 2 * t + h; };
 
   // c[q][i][e][h] += A(block s) * Bsrc(32 rows at byte offset bsrc of a
-  // row-major [k][kNC] swizzled buffer), k-steps alternating between the two
-  // partial sums q = kk & 1 (two independent DMMA chains per tile: half the
+  // row-major [k][kNC] swizzled buffer), k-step kk into partial sum
+  // q = kk % kParts (two independent DMMA chains per tile: half the
   // dependency latency of a leaf with few right-hand sides); the partial
   // sums are added once per row block.  Same order for every NC and WM.
-  double c[2][WM][E][2];
+  double c[kParts][WM][E][2];
+  auto csum = [&](int i, int e, int h) { return c[0][i][e][h] + c[1][i][e][h]; };
+  auto zero = [&](int i, int e, int h) {
+#pragma unroll
+    for (int q = 0; q < kParts; ++q) c[q][i][e][h] = 0.0;
+  };
   int s = 0;
   auto block_mma = [&](uint32_t bsrc) {
     if (!computes) return;
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
 #pragma unroll
       for (int i = 0; i < WM; ++i)
 #pragma unroll
-        for (int e = 0; e < E; ++e) dmma884(c[kk & 1][i][e][0], c[kk & 1][i][e][1], a[i][kk], bv[kk][e]);
+        for (int e = 0; e < E; ++e) dmma884(c[kk % kParts][i][e][0], c[kk % kParts][i][e][1], a[i][kk], bv[kk][e]);
     // The DMMAs have consumed every fragment loaded from the slot, so those
     // loads are complete: only now release the slot to the bulk-copy proxy.
     __syncwarp();
@@ -346,22 +357,22 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
     if (trsm) {
       for_c([&](int i, int e, int h) {
         c[0][i][e][h] = !computes ? 0.0 : -panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))];
-        c[1][i][e][h] = 0.0;
+        for (int q = 1; q < kParts; ++q) c[q][i][e][h] = 0.0;
       });
     } else {
-      for_c([&](int i, int e, int h) { c[0][i][e][h] = c[1][i][e][h] = 0.0; });
+      for_c([&](int i, int e, int h) { zero(i, e, h); });
     }
     for (int J = 0; J < I; ++J) block_mma(panel_u32 + static_cast<uint32_t>(J * kRB * kNC * 8));
     if (trsm) {
       // c = -(b_I - sum L'X); X_I = (-inv(L'_II)) * c
       if (computes)
-        for_c([&](int i, int e, int h) { cbuf[panel_idx<NC>(crow(i), ccol(e, h))] = c[0][i][e][h] + c[1][i][e][h]; });
+        for_c([&](int i, int e, int h) { cbuf[panel_idx<NC>(crow(i), ccol(e, h))] = csum(i, e, h); });
       named_sync(1, kThreads);
-      for_c([&](int i, int e, int h) { c[0][i][e][h] = c[1][i][e][h] = 0.0; });
+      for_c([&](int i, int e, int h) { zero(i, e, h); });
       block_mma(cbuf_u32);
       if (computes)
         for_c([&](int i, int e, int h) {
-          panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = c[0][i][e][h] + c[1][i][e][h];
+          panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = csum(i, e, h);
         });
       named_sync(1, kThreads);  // X_I visible; cbuf free
     } else {
@@ -370,7 +381,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
       named_sync(1, kThreads);
       if (computes)
         for_c([&](int i, int e, int h) {
-          panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = p.alpha * (c[0][i][e][h] + c[1][i][e][h]);
+          panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = p.alpha * csum(i, e, h);
         });
     }
   }

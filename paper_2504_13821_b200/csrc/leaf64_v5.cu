@@ -14,7 +14,7 @@
 //
 // Arithmetic: per element exactly v3's (leaf64_v3.cu) -- J ascending with the
 // diagonal block L'_II last, DMMA.8x8x4 k-steps alternating between two
-// partial sums, X = alpha * (c0 + c1) -- so v5 and v3 agree bit for bit and
+// partial sums kk % 2, X = alpha * (c0 + c1) -- so v5 and v3 agree bit for bit and
 // the launcher may pick either by right-hand-side count.
 //
 // Where it is used: direct trmm_base calls (a 256 x 2048 leaf: 13.6 us vs
@@ -180,12 +180,15 @@ __global__ void __launch_bounds__(kCW * 32 + 32, MINB) leaf5_trmm_kernel(const L
   for (int e = 0; e < E; ++e) b_base[e] = panel_u32 + 8u * static_cast<uint32_t>(pidx<NC>(t, 8 * e + g));
   constexpr uint32_t kRowBytes = NC * 8;
 
-  double c[2][4][E][2];
+  constexpr int kParts = 2;  // as leaf64_v3.cu
+  double c[kParts][4][E][2];
   auto zero_c = [&]() {
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int e = 0; e < E; ++e) c[0][mt][e][0] = c[0][mt][e][1] = c[1][mt][e][0] = c[1][mt][e][1] = 0.0;
+      for (int e = 0; e < E; ++e)
+#pragma unroll
+        for (int q = 0; q < kParts; ++q) c[q][mt][e][0] = c[q][mt][e][1] = 0.0;
   };
   zero_c();
   for (int s = 0; s < nsteps; ++s) {
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, MINB) leaf5_trmm_kernel(const L
         for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
           for (int e = 0; e < E; ++e)
-            dmma884(c[kk & 1][mt][e][0], c[kk & 1][mt][e][1], a[kk & 1][mt], bv[kk & 1][e]);
+            dmma884(c[kk % kParts][mt][e][0], c[kk % kParts][mt][e][1], a[kk & 1][mt], bv[kk & 1][e]);
       }
     }
     __syncwarp();
@@ -230,7 +233,8 @@ __global__ void __launch_bounds__(kCW * 32 + 32, MINB) leaf5_trmm_kernel(const L
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int r = r0 + 8 * mt + g, cc = 8 * e + 2 * t + h;
-            if (r < n && cc < ncols) *gaddr(r, cc) = p.alpha * (c[0][mt][e][h] + c[1][mt][e][h]);
+            if (r < n && cc < ncols)
+              *gaddr(r, cc) = p.alpha * (c[0][mt][e][h] + c[1][mt][e][h]);
           }
       zero_c();
     }
