@@ -31,6 +31,14 @@ import threading
 import time
 from pathlib import Path
 
+# Under torchrun, NCCL's communicator INIT lines go to a per-process file that
+# setup_dist() echoes to stderr (evidence of the rank count).  NCCL reads its
+# debug settings once, when the library initialises, so they are set before
+# torch is imported.
+if "WORLD_SIZE" in os.environ and "NCCL_DEBUG" not in os.environ:
+    os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT",
+                      NCCL_DEBUG_FILE=f"/tmp/rectri_bench_nccl.{os.getpid()}.log")
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -133,10 +141,7 @@ def setup_dist(args):
         if args.dry_gloo:
             dist.init_process_group("gloo")
         else:
-            nccl_log = None
-            if "NCCL_DEBUG" not in os.environ:  # communicator INIT lines, echoed to stderr below
-                nccl_log = f"/tmp/rectri_bench_nccl.{os.getpid()}.log"
-                os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,ENV", NCCL_DEBUG_FILE=nccl_log)
+            nccl_log = os.environ.get("NCCL_DEBUG_FILE")  # set at import (top of this file)
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             dist.barrier()

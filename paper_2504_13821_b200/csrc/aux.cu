@@ -227,4 +227,12 @@ double probe_peak_tflops(int kind) {
   return cudaGetLastError() == cudaSuccess ? flops / (best * 1e-3) / 1e12 : -1.0;
 }
 
+int smem_carveout_pct() {
+  static const int pct = [] {
+    const char* e = getenv("RECTRI_CU_SMEM_CARVEOUT");
+    return e ? atoi(e) : static_cast<int>(cudaSharedmemCarveoutMaxShared);
+  }();
+  return pct;
+}
+
 }  // namespace rectri_cu

@@ -57,4 +57,18 @@ __device__ __forceinline__ int swz64(int row, int col, int width) {
 
 __host__ __device__ __forceinline__ i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
 
+// Opts a kernel into `bytes` of dynamic shared memory and asks for the
+// largest shared-memory carveout of the SM's unified L1/shared storage, so
+// as many CTAs fit per SM as their shared memory allows (without it the
+// driver may pick a smaller carveout: ncu showed the 70 KB DGEMM CTA limited
+// to 2 per SM).  RECTRI_CU_SMEM_CARVEOUT overrides the percentage (-1: leave
+// the driver's choice).
+int smem_carveout_pct();
+template <typename Kern>
+inline void set_smem(Kern kern, int bytes) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  const int pct = smem_carveout_pct();
+  if (pct >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 }  // namespace rectri_cu

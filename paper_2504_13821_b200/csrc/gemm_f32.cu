@@ -434,7 +434,7 @@ template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB, int BK =
 void launch_cfg2(const GemmParams<float>& p, cudaStream_t s) {
   auto kern = sgemm_ffma2_kernel<BM, BN, STAGES, TA, TB, VA, VB, BK>;
   constexpr int smem = STAGES * BK * (BM + BN + 2 * kPadMC) * static_cast<int>(sizeof(float));
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  set_smem(kern, smem);
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
   kern<<<grid, 256, smem, s>>>(p);
   ++launch_counter();
@@ -445,7 +445,7 @@ void launch_cfg(const GemmParams<float>& p, cudaStream_t s) {
   auto kern = sgemm_ffma_kernel<BM, BN, STAGES, TA, TB, VA, VB>;
   constexpr int smem =
       STAGES * (FLayout<BM, TA>::ELEMS + FLayout<BN, !TB>::ELEMS) * static_cast<int>(sizeof(float));
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  set_smem(kern, smem);
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
   kern<<<grid, (BM / 8) * (BN / 8), smem, s>>>(p);
   ++launch_counter();

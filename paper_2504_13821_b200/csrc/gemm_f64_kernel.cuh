@@ -320,7 +320,7 @@ struct Config {
     auto kern = dgemm_dmma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TA, TB, VEC, MCMODE>;
     constexpr int pad = MCMODE == 1 ? 4 : 0;
     constexpr int smem = STAGES * (BM + BN + 2 * pad) * BK * static_cast<int>(sizeof(double));
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set_smem(kern, smem);
     const unsigned grid = static_cast<unsigned>(ceil_div(p.M, BM) * ceil_div(p.N, BN));
     kern<<<grid, WARPS_M * WARPS_N * 32, smem, s>>>(p);
     ++launch_counter();

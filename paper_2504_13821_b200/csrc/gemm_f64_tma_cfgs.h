@@ -19,7 +19,7 @@ struct Config {
     constexpr int slot_a = ((MC_A ? BM + 4 : BM) * kBK * 8 + 1023) / 1024 * 1024;
     constexpr int slot_b = ((MC_B ? BN + 4 : BN) * kBK * 8 + 1023) / 1024 * 1024;
     constexpr int smem = STAGES * (slot_a + slot_b) + 16 * STAGES + 1024;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set_smem(kern, smem);
     const unsigned grid = static_cast<unsigned>(ceil_div(p.M, BM) * ceil_div(p.N, BN));
     constexpr int threads = (WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32;
     kern<<<grid, threads, smem, s>>>(ma, mb, p);

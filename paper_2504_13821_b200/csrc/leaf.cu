@@ -468,7 +468,7 @@ void launch_leaf(const LeafParams<T>& p_in, cudaStream_t s) {
   LeafParams<T> p = p_in;
   p.debug_skip = leaf_debug();
   const int smem = static_cast<int>(LeafSmem<T>::total * sizeof(T));
-  cudaFuncSetAttribute(leaf_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  set_smem(leaf_kernel<T>, smem);
   const unsigned grid = static_cast<unsigned>(ceil_div(p.nrhs, kNC));
   leaf_kernel<T><<<grid, kThreads, smem, s>>>(p);
   ++launch_counter();

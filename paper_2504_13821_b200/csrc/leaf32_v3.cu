@@ -353,7 +353,7 @@ void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t
     ++launch_counter();
   }
   auto go = [&](auto kern, int width, int smem) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set_smem(kern, smem);
     kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), 4 * width + 32, smem, s>>>(p, scratch);
   };
   const int nc = leaf3_width(p.nrhs, p.trsm != 0);

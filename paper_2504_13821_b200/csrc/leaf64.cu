@@ -524,7 +524,7 @@ void launch_leaf_f64(const LeafParams<double>& p, cudaStream_t s) {
     ++launch_counter();
   }
   const int smem = static_cast<int>(sizeof(Smem));
-  cudaFuncSetAttribute(leaf64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  set_smem(leaf64_kernel, smem);
   const unsigned grid = static_cast<unsigned>(ceil_div(p.nrhs, kNC));
   const char* tr = getenv("RECTRI_CU_LEAF_TRACE");
   if (tr && atoi(tr)) {  // diagnostics: per-CTA phase stamps, summary on stderr

@@ -448,7 +448,7 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
   }
   const int nc = leaf3_width(p.nrhs, p.trsm != 0);
   auto go = [&](auto kern, int width, int smem) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set_smem(kern, smem);
     kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), kThreads + 32, smem, s>>>(p, scratch);
   };
   const char* wm = getenv("RECTRI_CU_LEAF_WM");

@@ -245,7 +245,7 @@ template <int NC, int STAGES, int MINB>
 void go(const LeafParams<double>& p, const double* P, cudaStream_t s) {
   auto kern = leaf5_trmm_kernel<NC, STAGES, MINB>;
   constexpr int smem = smem_bytes<NC, STAGES>();
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  set_smem(kern, smem);
   kern<<<static_cast<unsigned>(ceil_div(p.nrhs, NC)), kCW * 32 + 32, smem, s>>>(p, P);
   ++launch_counter();
 }

@@ -364,7 +364,7 @@ template <bool A_MN, bool B_MN, int BK>
 void launch(const CUtensorMap* maps, const GemmParams<float>& p, cudaStream_t s) {
   auto kern = tf32x3_kernel<A_MN, B_MN, BK>;
   constexpr int smem = Geo<BK>::SMEM;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  set_smem(kern, smem);
   const unsigned grid = static_cast<unsigned>(ceil_div(p.M, BM) * ceil_div(p.N, BN));
   // MN-major descriptor offsets: LBO = 32-element chunk stride, SBO = 4-row k-group stride
   const uint32_t lbo = Geo<BK>::MN_CHUNK, sbo = 512;
