@@ -102,10 +102,13 @@ __device__ __forceinline__ void lds128(double& x, double& y, uint32_t a) {
 // PRODUCER: a dedicated 32-thread producer warp (else lane 0 of warp 0).
 // MC_A: A tile outer(m)-contiguous (op(A) = A); MC_B: B tile outer(n)-contiguous
 // (op(B) = B^T).
+// One BM x BN output tile at (m0, n0) (the body of every TMA DGEMM kernel).
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B>
-__global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32, 1)
-    dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
-                     const __grid_constant__ CUtensorMap mapB, const GemmParams<double> p) {
+__device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const CUtensorMap* mapB_,
+                                               const GemmParams<double>& p, const int m0, const int n0,
+                                               unsigned char* smem_raw) {
+  const CUtensorMap& mapA = *mapA_;
+  const CUtensorMap& mapB = *mapB_;
   constexpr int NCW = WARPS_M * WARPS_N;  // consumer warps
   constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
   constexpr int TM = WM / 16, TN = WN / 8;
@@ -117,7 +120,6 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
   constexpr uint32_t A_SLOT = (A_BYTES + 1023u) & ~1023u, B_SLOT = (B_BYTES + 1023u) & ~1023u;
   constexpr uint32_t STAGE_BYTES = A_SLOT + B_SLOT;
 
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for the 128-byte swizzle atoms.
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -129,18 +131,6 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  // Grouped rasterization (as the cp.async kernel): consecutive CTAs walk 16
-  // M-tiles down one N column so resident CTAs share panels in L2.
-  constexpr int kGroup = 16;
-  const int tiles_m = static_cast<int>(ceil_div(p.M, BM));
-  const int tiles_n = static_cast<int>(ceil_div(p.N, BN));
-  const int lin = static_cast<int>(blockIdx.x);
-  const int per_group = kGroup * tiles_n;
-  const int grp = lin / per_group, in_grp = lin - grp * per_group;
-  const int gm0 = grp * kGroup;
-  const int gsize = min(kGroup, tiles_m - gm0);
-  const int tm = gm0 + in_grp % gsize, tn = in_grp / gsize;
-  const int m0 = tm * BM, n0 = tn * BN;
   const int KT = static_cast<int>(ceil_div(p.K, kBK));
 
   if (threadIdx.x == 0) {
@@ -293,6 +283,55 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
           }
         }
     }
+}
+
+// Grouped rasterization (as the cp.async kernel): consecutive CTAs walk 16
+// M-tiles down one N column so resident CTAs share panels in L2.
+__device__ __forceinline__ void grouped_tile(int lin, int tiles_m, int tiles_n, int& tm, int& tn) {
+  constexpr int kGroup = 16;
+  const int per_group = kGroup * tiles_n;
+  const int grp = lin / per_group, in_grp = lin - grp * per_group;
+  const int gm0 = grp * kGroup;
+  const int gsize = min(kGroup, tiles_m - gm0);
+  tm = gm0 + in_grp % gsize;
+  tn = in_grp / gsize;
+}
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B>
+__global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32, 1)
+    dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapB, const GemmParams<double> p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  int tm, tn;
+  grouped_tile(static_cast<int>(blockIdx.x), static_cast<int>(ceil_div(p.M, BM)), static_cast<int>(ceil_div(p.N, BN)),
+               tm, tn);
+  dgemm_tma_tile<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B>(&mapA, &mapB, p, tm * BM, tn * BN, smem_raw);
+}
+
+// Wave-tail split: the columns [0, n_main) in 64x64 tiles -- a whole number
+// of waves of resident CTAs -- and the remaining columns in 32x32 tiles, four
+// CTAs per 64x64 tile, so the last wave is not a few long CTAs on a mostly
+// idle GPU.  Every element keeps the same k-tile order, so the result is bit
+// for bit that of the uniform kernels.
+template <bool MC_A, bool MC_B>
+__global__ void __launch_bounds__(5 * 32, 1)
+    dgemm_tma_split_kernel(const __grid_constant__ CUtensorMap a64, const __grid_constant__ CUtensorMap b64,
+                           const __grid_constant__ CUtensorMap a32, const __grid_constant__ CUtensorMap b32,
+                           const GemmParams<double> p, const int n_main) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int tiles_m64 = static_cast<int>(ceil_div(p.M, 64));
+  const int main_tiles = tiles_m64 * (n_main / 64);
+  const int b = static_cast<int>(blockIdx.x);
+  if (b < main_tiles) {
+    int tm, tn;
+    grouped_tile(b, tiles_m64, n_main / 64, tm, tn);
+    dgemm_tma_tile<64, 64, 2, 2, 4, true, MC_A, MC_B>(&a64, &b64, p, tm * 64, tn * 64, smem_raw);
+  } else {
+    const int tiles_m32 = static_cast<int>(ceil_div(p.M, 32));
+    const int r = b - main_tiles;
+    dgemm_tma_tile<32, 32, 2, 2, 4, true, MC_A, MC_B>(&a32, &b32, p, (r % tiles_m32) * 32,
+                                                     n_main + (r / tiles_m32) * 32, smem_raw);
+  }
 }
 
 }  // namespace dgemm_tma

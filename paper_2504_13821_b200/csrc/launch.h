@@ -58,6 +58,8 @@ struct LeafParams {
 constexpr int kLeafMax = 256;
 
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s);
+// 64x64 tiles with the last, short wave's columns in 32x32 tiles (same bits).
+bool launch_gemm_f64_split(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s);
 void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s);
 // fp32 3xTF32 variant on tcgen05 (sgemm_tf32x3.cu), opt-in: RECTRI_CU_FP32_TF32X3=1.
 bool tf32x3_enabled();

@@ -188,3 +188,32 @@ def test_sgemm_v2_vector_epilogue_bitwise(cuda, ta, tb, monkeypatch):
             outs.append(to_np(C))
         assert oracle.bitwise_equal(outs[0], outs[1]), (M, N, K, beta)
 
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_wave_tail_split_bitwise(cuda, ta, tb, monkeypatch):
+    """The wave-tail split kernel (64x64 tiles for the leading columns, 32x32
+    tiles for the last wave's) keeps every element's k-tile order: bit for
+    bit the uniform 64x64 kernel (RECTRI_CU_GEMM64_TMA=2), ragged M / N / K,
+    beta 0 and not; RECTRI_CU_GEMM64_SPLIT=2 forces the split at N / 2."""
+    rng = np.random.default_rng(41 + 2 * ta + tb)
+    for (M, N, K), beta in itertools.product(((2048, 2048, 1024), (130, 300, 50), (2000, 2100, 300), (77, 129, 1100)),
+                                             (1.0, 0.0)):
+        a = F(rng.uniform(-1, 1, (K, M) if ta else (M, K)))
+        b = F(rng.uniform(-1, 1, (N, K) if tb else (K, N)))
+        c0 = F(rng.uniform(-1, 1, (M, N)))
+        A, B = to_dev(a), to_dev(b)
+        outs = []
+        for env in ({"RECTRI_CU_GEMM64_TMA": "2"}, {"RECTRI_CU_GEMM64_SPLIT": "2"}):
+            monkeypatch.delenv("RECTRI_CU_GEMM64_TMA", raising=False)
+            monkeypatch.delenv("RECTRI_CU_GEMM64_SPLIT", raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            C = to_dev(c0)
+            gemm(-1.0, Trans(ta), A.cview(), Trans(tb), B.cview(), beta, C.view())
+            outs.append(to_np(C))
+        assert oracle.bitwise_equal(outs[0], outs[1]), (M, N, K, beta)
+        opa = a.T if ta else a
+        opb = b.T if tb else b
+        ref = -(opa @ opb) + beta * c0
+        assert np.max(np.abs(outs[1] - ref)) <= 2 * K * np.finfo(float).eps * np.max(np.abs(opa) @ np.abs(opb) + 1)

@@ -172,3 +172,26 @@ def test_nonfinite_rhs_row_propagation(cuda, monkeypatch, version):
     assert np.all(np.isfinite(got[:, others]))
     monkeypatch.delenv("RECTRI_CU_LEAF")
     rc.clear_graph_cache()
+
+
+def test_pageable_host_operands_singular_and_exact(cuda):
+    """Pageable (plain numpy / CPU-tensor) A and B go through the pinned
+    bounce staging: bitwise the device-resident result, and a zero pivot
+    still raises SingularityError with its global row (the staging drains
+    before the error surfaces)."""
+    s = oracle.spec(0, 0, 0, 0, 1.0)
+    n, m = 1500, 2300
+    a = oracle.make_dominant(n, 0, 70)
+    b = oracle.make_random(n, m, 71)
+    want = run_op("trsm", s, a, b, 256)
+    A = rc.MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(a)), device="cpu")
+    B = rc.MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(b)), device="cpu")
+    rec_trsm(tspec(s), A.cview(), B.view(), Threshold(256), Backend.cuda(device=0))
+    assert oracle.bitwise_equal(to_np(B), want)
+    a2 = a.copy()
+    a2[777, 777] = 0.0
+    A2 = rc.MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(a2)), device="cpu")
+    B2 = rc.MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(b)), device="cpu")
+    with pytest.raises(SingularityError) as e:
+        rec_trsm(tspec(s), A2.cview(), B2.view(), Threshold(256), Backend.cuda(device=0))
+    assert e.value.index() == 777
