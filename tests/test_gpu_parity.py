@@ -413,3 +413,36 @@ def test_host_streamed_time_panels(cuda, op, monkeypatch):
         dev = run_op(op, s, a, b, 128)
         host = run_op(op, s, a, b, 128, device="cpu")
         assert oracle.bitwise_equal(dev, host), (side, uplo, trans, diag)
+
+
+@pytest.mark.parametrize("side,uplo,trans", list(__import__("itertools").product((0, 1), (0, 1), (0, 1))))
+def test_trsm_non_dominant_well_conditioned(cuda, monkeypatch, side, uplo, trans):
+    """The default leaf applies explicit inverses of its 32x32 diagonal blocks
+    (leaf64_v3.cu) instead of the reference's substitution; every other test
+    uses diagonally dominant triangles.  Here A is the Cholesky factor of an
+    SPD matrix with eigenvalues in [1, 100] -- condition number about 10, far
+    from diagonally dominant (off-diagonal row sums exceed the diagonal).
+    The result must pass the reference's residual criterion and agree with
+    the reference-order leaf (RECTRI_CU_LEAF=2) to a cond-scaled forward bound."""
+    import paper_2504_13821_b200 as rc
+
+    n, m = 768, 300
+    rng = np.random.default_rng(900 + 4 * side + 2 * uplo + trans)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    spd = (q * np.logspace(0, 2, n)) @ q.T
+    low = np.linalg.cholesky(spd)
+    a = F(low if uplo == 0 else low.T)
+    offsum = np.abs(np.tril(low, -1)).sum(1)
+    assert np.mean(offsum > np.abs(np.diag(low))) > 0.5  # not diagonally dominant
+    s = oracle.spec(side, uplo, trans, 0, 1.0)
+    b = F(rng.uniform(-1, 1, (n, m) if side == 0 else (m, n)))
+    got = run_op("trsm", s, a, b, 256)
+    check_against_oracle("trsm", s, a, b, got)
+    monkeypatch.setenv("RECTRI_CU_LEAF", "2")
+    rc.clear_graph_cache()
+    ref_order = run_op("trsm", s, a, b, 256)
+    monkeypatch.delenv("RECTRI_CU_LEAF")
+    rc.clear_graph_cache()
+    cond = np.linalg.cond(low)
+    err = np.max(np.abs(got - ref_order)) / np.max(np.abs(ref_order))
+    assert err <= 64 * n * np.finfo(float).eps * cond, (err, cond)
