@@ -35,7 +35,8 @@ from pathlib import Path
 # setup_dist() echoes to stderr (evidence of the rank count).  NCCL reads its
 # debug settings once, when the library initialises, so they are set before
 # torch is imported.
-if "WORLD_SIZE" in os.environ and "NCCL_DEBUG" not in os.environ:
+# (An inherited NCCL_DEBUG=VERSION / WARN is raised to INFO for INIT only.)
+if "WORLD_SIZE" in os.environ and os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
     os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT",
                       NCCL_DEBUG_FILE=f"/tmp/rectri_bench_nccl.{os.getpid()}.log")
 
