@@ -371,10 +371,6 @@ class Recursion {
   size_t packed_stride = 0;
   int pack_asc = 0;  // TRMM triangles packed in ascending order (v5 leaf)
   int leaf_idx = 0;
-  // Recorded on the stream right after the lag_leaves-th leaf is enqueued
-  // (the next right-hand-side panel starts there: see build()).
-  cudaEvent_t lag_event = nullptr;
-  int lag_leaves = 0;
   ConcCtx<T>* conc = nullptr;
 
   // Scratch elements the concurrent TRMM nodes of run(n, rhs) use.
@@ -397,8 +393,6 @@ class Recursion {
       else if (!dry_)
         enqueue_base<T>(op_, spec, A, B, s_, packed ? packed + leaf_idx * packed_stride : nullptr, pack_asc);
       ++leaf_idx;
-      if (lag_event && !dry_ && !kernels && leaf_idx == lag_leaves)
-        cuda_check(cudaEventRecord(lag_event, s_), "record lag");
       return;
     }
     const i64 mid = n / 2;  // split_half
@@ -921,27 +915,15 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
     cudaEvent_t fork = ev();
     cuda_check(cudaEventRecord(fork, s), "record fork");
     const i64 w = ((rhs + P - 1) / P + 63) / 64 * 64;
-    // Panel k starts once panel k-1 has run its first `lag` leaves
-    // (RECTRI_CU_STREAM_LAG, default 0): the panels' identical kernel
-    // sequences then run out of phase, a leaf of one beside a GEMM of the
-    // other instead of leaf beside leaf.  Only the start order changes.
-    int lag = 0;
-    if (const char* e = getenv("RECTRI_CU_STREAM_LAG")) lag = std::max(0, atoi(e));
-    cudaEvent_t prev_lag = nullptr;
     for (int k = 0; k < P; ++k) {
       const i64 r0 = k * w;
       if (r0 >= rhs) break;
       const i64 wi = r0 + w <= rhs ? w : rhs - r0;
       const DView<T> panel = left ? B.sub(0, r0, B.rows, wi) : B.sub(r0, 0, wi, B.cols);
       cudaStream_t sk = k == 0 ? s : res.aux[k - 1];
-      if (k > 0) cuda_check(cudaStreamWaitEvent(sk, prev_lag ? prev_lag : fork, 0), "wait fork");
+      if (k > 0) cuda_check(cudaStreamWaitEvent(sk, fork, 0), "wait fork");
       Recursion<T> rec(op, threshold, sk, nullptr, nullptr);
-      if (lag > 0 && k + 1 < P) {
-        rec.lag_event = ev();
-        rec.lag_leaves = lag;
-      }
       with_packs(rec).run(eff, A, panel, 0);
-      prev_lag = rec.lag_event && rec.leaf_idx >= lag ? rec.lag_event : nullptr;
       if (k > 0) {
         cudaEvent_t join = ev();
         cuda_check(cudaEventRecord(join, sk), "record join");
