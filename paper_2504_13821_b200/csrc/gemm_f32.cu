@@ -317,17 +317,46 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc2[i][j] = 0ull;
 
-#pragma unroll
-  for (int s = 0; s < STAGES; ++s) {
-    if (s < KT) {
-      la.load(sA + s * A_EL, s);
-      lb.load(sB + s * B_EL, s);
+  // Stage s holds k-tile j with j % STAGES == s.  full[s]: every thread's
+  // cp.async copies of the tile have landed (cp.async.mbarrier.arrive.noinc,
+  // 256 arrivals); empty[s]: all 8 warps have read the tile.  Instead of a
+  // CTA barrier per k-tile, the refill of a stage is issued one tile later
+  // than it could be -- at the end of tile kt the stage of tile kt - 1 gets
+  // tile kt + STAGES - 1 -- so the empty wait is normally already satisfied
+  // and warps drift apart freely; the refill still has a whole tile of
+  // compute to land in.
+  static_assert(STAGES >= 3, "the deferred refill needs three stages");
+  __shared__ __align__(8) unsigned long long bars[2 * STAGES];
+  const uint32_t full0 = smem_u32(&bars[0]), empty0 = smem_u32(&bars[STAGES]);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < STAGES; ++q) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(full0 + 8 * q), "r"(NT));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(empty0 + 8 * q), "r"(NT / 32));
     }
-    cp_async_commit();
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  cp_async_wait<STAGES - 1>();
   __syncthreads();
+  auto bar_wait = [](uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          " selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(ok)
+          : "r"(bar), "r"(parity)
+          : "memory");
+  };
+  auto fill = [&](int stage, i64 tile) {  // this thread's copies of k-tile `tile`, then its arrival
+    la.load(sA + stage * A_EL, tile);
+    lb.load(sB + stage * B_EL, tile);
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(full0 + 8 * stage) : "memory");
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES; ++s)
+    if (s < KT) fill(s, s);
   float fa[2][8], fb[2][8];
+  bar_wait(full0, 0);
   read_k<BM>(sA, ty, 0, fa[0]);
   read_k<BN>(sB, tx, 0, fb[0]);
   int st = 0;
@@ -341,16 +370,20 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
         read_k<BM>(a_s, ty, k + 1, fa[cb ^ 1]);
         read_k<BN>(b_s, tx, k + 1, fb[cb ^ 1]);
       } else {
-        // every thread has read tile kt: refill its stage, move to kt + 1
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        if (kt + STAGES < KT) {
-          la.load(sA + st * A_EL, kt + STAGES);
-          lb.load(sB + st * B_EL, kt + STAGES);
+        // this warp has read tile kt
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(empty0 + 8 * st) : "memory");
+        // refill the stage of tile kt - 1 with tile kt + STAGES - 1
+        const i64 nt = kt + STAGES - 1;
+        if (kt >= 1 && nt < KT) {
+          const int rs = static_cast<int>((kt - 1) % STAGES);
+          bar_wait(empty0 + 8 * rs, static_cast<uint32_t>(((kt - 1) / STAGES) & 1));
+          fill(rs, nt);
         }
-        cp_async_commit();
         st = st + 1 == STAGES ? 0 : st + 1;
         if (kt + 1 < KT) {
+          bar_wait(full0 + 8 * st, static_cast<uint32_t>(((kt + 1) / STAGES) & 1));
           read_k<BM>(sA + st * A_EL, ty, 0, fa[cb ^ 1]);
           read_k<BN>(sB + st * B_EL, tx, 0, fb[cb ^ 1]);
         }

@@ -15,7 +15,7 @@ N = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
 be = Backend.cuda(flags=NO_GRAPH)
 res = []
 for MK in (8192, 4096, 2048, 1024, 512, 256, 128, 64):
-    for ta, tb, tag in ((0, 0, "NN"), (1, 0, "TN"), (0, 1, "NT")):
+    for ta, tb, tag in ((0, 0, "NN"), (1, 0, "TN"), (0, 1, "NT"), (1, 1, "TT")):
         M = K = MK
         A = MatrixBuffer(K if ta else M, M if ta else K, dt, "cuda")
         B = MatrixBuffer(N, K, dt, "cuda") if tb else MatrixBuffer(K, N, dt, "cuda")
