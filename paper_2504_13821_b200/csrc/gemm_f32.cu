@@ -75,6 +75,21 @@ struct FLoader {
   __device__ __forceinline__ void load(float* s, i64 kt) const {
     const int k0 = static_cast<int>(kt * BKT);
     const float* tb = p0 + (KC ? static_cast<i64>(k0) : static_cast<i64>(k0) * ld);
+    // interior tiles (the vast majority): no per-copy bounds, the source
+    // pointer advanced by one add per copy instead of a multiply
+    const bool inside = KC ? (k0 + BKT <= k_lim && o_lim >= BO) : (k0 + BKT <= k_lim && fix_bytes == VEC * 4);
+    if (inside) {
+      const float* g = tb;
+#pragma unroll
+      for (int it = 0; it < IT; ++it, g += step) {
+        const int row = row0 + it * STEP;
+        float* dst = KC ? s + row * kRowKC + col : s + row * (BO + kPadMC) + col;
+        if constexpr (VEC == 4) cp_async16(dst, g, 16);
+        else if constexpr (VEC == 2) cp_async8(dst, g, 8);
+        else cp_async4(dst, g, 4);
+      }
+      return;
+    }
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int row = row0 + it * STEP;
@@ -270,6 +285,14 @@ struct TLoaderKC {
   }
   __device__ __forceinline__ void load(float* s, i64 kt) const {
     const int k0 = static_cast<int>(kt * BK);
+    if (k0 + BK <= k_lim && o_lim >= BO) {  // interior tile: no per-copy bounds
+      const float* g = p0 + k0;
+#pragma unroll
+      for (int ob = 0; ob < BO / 32; ++ob, g += step32)
+#pragma unroll
+        for (int h = 0; h < BK / 8; ++h) cp_async4(s + (kl + 8 * h) * RS + ol + 32 * ob, g + 8 * h, 4);
+      return;
+    }
 #pragma unroll
     for (int h = 0; h < BK / 8; ++h)
 #pragma unroll
