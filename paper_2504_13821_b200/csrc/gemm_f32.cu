@@ -57,7 +57,7 @@ struct FLoader {
   const float* p0;
   i64 ld, step;
   int row0, col;
-  int o_lim, k_lim, fix_bytes;
+  int o_lim, k_lim, fix_bytes, soff;
 
   __device__ void init(const float* X, i64 ld_, i64 o0, i64 O, i64 K) {
     ld = ld_;
@@ -70,6 +70,7 @@ struct FLoader {
     step = static_cast<i64>(STEP) * ld;
     const int rem = o_lim - col;
     fix_bytes = rem >= VEC ? VEC * 4 : (rem > 0 ? rem * 4 : 0);
+    soff = KC ? row0 * kRowKC + col : row0 * (BO + kPadMC) + col;
   }
 
   __device__ __forceinline__ void load(float* s, i64 kt) const {
@@ -82,8 +83,7 @@ struct FLoader {
       const float* g = tb;
 #pragma unroll
       for (int it = 0; it < IT; ++it, g += step) {
-        const int row = row0 + it * STEP;
-        float* dst = KC ? s + row * kRowKC + col : s + row * (BO + kPadMC) + col;
+        float* dst = s + soff + it * STEP * (KC ? kRowKC : BO + kPadMC);
         if constexpr (VEC == 4) cp_async16(dst, g, 16);
         else if constexpr (VEC == 2) cp_async8(dst, g, 8);
         else cp_async4(dst, g, 4);
@@ -272,11 +272,12 @@ struct TLoaderKC {
   const float* base;
   const float* p0;
   i64 step32;
-  int kl, ol, o_lim, k_lim;
+  int kl, ol, o_lim, k_lim, soff;
 
   __device__ void init(const float* X, i64 ld, i64 o0, i64 O, i64 K) {
     kl = threadIdx.x % 8;
     ol = threadIdx.x / 8;
+    soff = kl * RS + ol;  // this thread's element of a stage, constant offsets from here
     o_lim = static_cast<int>(O - o0 < (1 << 30) ? O - o0 : (1 << 30));
     k_lim = static_cast<int>(K < (1 << 30) ? K : (1 << 30));
     base = X + o0 * ld;
@@ -287,10 +288,11 @@ struct TLoaderKC {
     const int k0 = static_cast<int>(kt * BK);
     if (k0 + BK <= k_lim && o_lim >= BO) {  // interior tile: no per-copy bounds
       const float* g = p0 + k0;
+      float* d = s + soff;
 #pragma unroll
       for (int ob = 0; ob < BO / 32; ++ob, g += step32)
 #pragma unroll
-        for (int h = 0; h < BK / 8; ++h) cp_async4(s + (kl + 8 * h) * RS + ol + 32 * ob, g + 8 * h, 4);
+        for (int h = 0; h < BK / 8; ++h) cp_async4(d + 8 * h * RS + 32 * ob, g + 8 * h, 4);
       return;
     }
 #pragma unroll

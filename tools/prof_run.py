@@ -28,14 +28,14 @@ if kind in ("trsm", "trmm", "strsm"):
     rc.fill_uniform(B.view(), seed=2)
     fn = rc.rec_trmm if kind == "trmm" else rc.rec_trsm
     fn(TriangularSpec(), A.cview(), B.view(), Threshold(t), be)
-elif kind in ("gemm", "gemmtn", "sgemm", "tf32x3"):
+elif kind in ("gemm", "gemmtn", "sgemm", "sgemmtn", "tf32x3"):
     M, N, K = args
-    if kind in ("sgemm", "tf32x3"):
+    if kind in ("sgemm", "sgemmtn", "tf32x3"):
         f64 = torch.float32
     if kind == "tf32x3":
         be = Backend.cuda(flags=NO_GRAPH | rc.TF32X3)
-    ta = Trans.Trans if kind == "gemmtn" else Trans.NoTrans
-    A = MatrixBuffer(K, M, f64, "cuda") if kind == "gemmtn" else MatrixBuffer(M, K, f64, "cuda")
+    ta = Trans.Trans if kind in ("gemmtn", "sgemmtn") else Trans.NoTrans
+    A = MatrixBuffer(K, M, f64, "cuda") if ta == Trans.Trans else MatrixBuffer(M, K, f64, "cuda")
     B = MatrixBuffer(K, N, f64, "cuda")
     C = MatrixBuffer(M, N, f64, "cuda")
     for i, x in enumerate((A, B, C)):
