@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
   read_k<BN>(sB, tx, 0, fb[0]);
   int st = 0;
   for (i64 kt = 0; kt < KT; ++kt) {
+    const int cur = st;
     const float* a_s = sA + st * A_EL;
     const float* b_s = sB + st * B_EL;
 #pragma unroll
@@ -395,11 +396,7 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
         read_k<BM>(a_s, ty, k + 1, fa[cb ^ 1]);
         read_k<BN>(b_s, tx, k + 1, fb[cb ^ 1]);
       } else {
-        // this warp has read tile kt
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0)
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(empty0 + 8 * st) : "memory");
-        // refill the stage of tile kt - 1 with tile kt + STAGES - 1
+        // refill the stage of tile kt - 1 (released after its last FFMAs) with tile kt + STAGES - 1
         const i64 nt = kt + STAGES - 1;
         if (kt >= 1 && nt < KT) {
           const int rs = static_cast<int>((kt - 1) % STAGES);
@@ -425,6 +422,11 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
         }
       }
     }
+    // this warp's last reads of tile kt have been consumed by the FFMAs above
+    // (so they are complete): release the stage
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(empty0 + 8 * cur) : "memory");
   }
   cp_async_wait<0>();
 

@@ -27,10 +27,16 @@ def _san(tool, args, env_extra=None):
                                   ["trsm", "300", "40", "64"], ["sgemm", "130", "70", "50"], ["sgemm", "256", "200", "300"],
                                   ["leaf32", "100", "70"], ["strsm", "300", "40", "64"], ["trmm", "520", "40", "32"]])
 def test_kernels_clean(cuda, tool, args):
-    # racecheck does not model mbarrier-ordered cp.async.bulk ring refills
-    # (the default fp64 leaf, leaf64_v3.cu, reports its ring as a hazard); it
-    # checks the barrier-synchronised v2 leaf, the other tools the default.
-    env = {"RECTRI_CU_LEAF": "2"} if tool == "racecheck" and "gemm" not in args[0] else None
+    # racecheck does not model mbarrier-ordered refills (the default fp64
+    # leaf's bulk-copy ring, leaf64_v3.cu, and the fp32 GEMM's per-stage
+    # cp.async mbarriers, gemm_f32.cu, report as hazards); it checks the
+    # barrier-synchronised v2 leaf and v1 fp32 GEMM, the other tools the
+    # defaults, whose ordering test_gpu_leaf.py / test_gpu_gemm.py stress.
+    env = None
+    if tool == "racecheck" and "gemm" not in args[0]:
+        env = {"RECTRI_CU_LEAF": "2", "RECTRI_CU_SGEMM": "1"}
+    elif tool == "racecheck" and args[0] == "sgemm":
+        env = {"RECTRI_CU_SGEMM": "1"}
     r = _san(tool, args, env)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-3000:]
