@@ -116,35 +116,6 @@ struct BackendInfo {
   unsigned flags = 0;
 };
 
-// Latency-bound fp64 TRSM calls (n <= RECTRI_CU_SPLITK_MAXN, default 2048)
-// run every TMA-fed GEMM update with K split across a 2-CTA cluster
-// (GemmParams::split_k): the dependency chain X1 -> GEMM -> X2 is the whole
-// call there, and the split halves each update's k-chain.  Decided once per
-// call from the caller's own views (n, alignment, leading dimensions), so the
-// device, host-staged and column-sharded forms of a call compute identical
-// bits; it changes the summation (low half + high half) against a call
-// without it, within the reference tolerance.
-thread_local int t_split_k = 0;
-struct SplitKScope {
-  explicit SplitKScope(int v) { t_split_k = v; }
-  ~SplitKScope() { t_split_k = 0; }
-};
-template <typename T>
-int latency_split_k(int op, const rectri_cu_view& Av, const rectri_cu_view& Bv) {
-  if (!std::is_same<T, double>::value || op != 1 /* kTrsm */) return 0;
-  static const long long maxn = [] {
-    const char* e = getenv("RECTRI_CU_SPLITK_MAXN");
-    return e ? atoll(e) : 2048LL;
-  }();
-  const auto al16 = [](const void* x, i64 off) {
-    return ((reinterpret_cast<uintptr_t>(x) + static_cast<uintptr_t>(off) * sizeof(T)) & 15u) == 0;
-  };
-  const bool aligned = Av.origin_rows % 2 == 0 && Bv.origin_rows % 2 == 0 &&
-                       al16(Av.origin, Av.col_offset * Av.origin_rows + Av.row_offset) &&
-                       al16(Bv.origin, Bv.col_offset * Bv.origin_rows + Bv.row_offset);
-  return Av.rows <= maxn && aligned ? 2 : 0;
-}
-
 // RECTRI_CU_TF32X3 for the duration of one fp32 call on this thread.
 struct Tf32x3Scope {
   explicit Tf32x3Scope(bool on) { tf32x3_set_call(on); }
@@ -327,7 +298,7 @@ void enqueue_gemm(T alpha, bool ta, DView<const T> A, bool tb, DView<const T> B,
       K<T>::scale(C.p, C.ld, M, N, beta, s);
     return;
   }
-  GemmParams<T> p{M, N, Kd, alpha, beta, A.p, A.ld, B.p, B.ld, C.p, C.ld, busy_gpu, t_split_k};
+  GemmParams<T> p{M, N, Kd, alpha, beta, A.p, A.ld, B.p, B.ld, C.p, C.ld, busy_gpu};
   ProfScope prof(0, 2.0 * static_cast<double>(M) * N * Kd, s);
   K<T>::gemm(p, ta, tb, s);
 }
@@ -1008,7 +979,7 @@ std::shared_ptr<GraphEntry> enqueue_device(OpK op, const Spec& spec, DView<const
       if (sink) sink(user, e.e, e.n, e.m);
     return g;
   }
-  const int mode = dtype_code<T>() + (std::is_same<T, float>::value && tf32x3_enabled() ? 10 : 0) + 100 * t_split_k;
+  const int mode = dtype_code<T>() + (std::is_same<T, float>::value && tf32x3_enabled() ? 10 : 0);
   const Key key{static_cast<int>(op), mode, spec.side, spec.uplo, spec.trans,
                 spec.diag, bits_of(spec.alpha), static_cast<const void*>(A.p), A.ld, A.rows,
                 static_cast<void*>(B.p), B.ld, B.rows, B.cols, threshold, dev};
@@ -1551,7 +1522,6 @@ void rec_entry(OpK op, const rectri_cu_spec* cspec, const rectri_cu_view& Av,
          side_name(spec.side));
   if (overlaps(Av, Bv)) fail(RECTRI_CU_ALIAS, "A and B views overlap");
   if (Av.rows == 0 || Bv.rows == 0 || Bv.cols == 0) return;
-  const SplitKScope split_scope(latency_split_k<T>(op == kTrsm ? 1 : 0, Av, Bv));
   const Nvtx range(op == kTrsm ? "rectri rec_trsm n=%lld rhs=%lld" : "rectri rec_trmm n=%lld rhs=%lld",
                    static_cast<long long>(Av.rows),
                    static_cast<long long>(spec.side == RECTRI_CU_LEFT ? Bv.cols : Bv.rows));

@@ -68,7 +68,7 @@ int choose_tma(const GemmParams<double>& p) {
 void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
   const int cfg = choose_tma(p);
-  if (cfg == 1 && p.split_k != 2 && launch_gemm_f64_split(p, ta, tb, s)) return;
+  if (cfg == 1 && launch_gemm_f64_split(p, ta, tb, s)) return;
   if (launch_gemm_f64_tma(p, ta, tb, s, cfg)) return;
   const bool vec2 = aligned16(p.A) && aligned16(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
   kRuns[choose(p)](p, ta, tb, vec2, s);

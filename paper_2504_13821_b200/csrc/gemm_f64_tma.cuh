@@ -103,13 +103,7 @@ __device__ __forceinline__ void lds128(double& x, double& y, uint32_t a) {
 // MC_A: A tile outer(m)-contiguous (op(A) = A); MC_B: B tile outer(n)-contiguous
 // (op(B) = B^T).
 // One BM x BN output tile at (m0, n0) (the body of every TMA DGEMM kernel).
-// SPLITK = 2: the tile's k-tiles are split between the two CTAs of a
-// cluster (rank 0: the first ceil(KT/2), rank 1: the rest); rank 1 hands its
-// accumulator to rank 0 through distributed shared memory and rank 0 adds it
-// (low k + high k, a fixed order) before the epilogue.  Deterministic for a
-// given K, used for whole latency-bound calls (GemmParams::split_k).
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B,
-          int SPLITK = 1>
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B>
 __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const CUtensorMap* mapB_,
                                                const GemmParams<double>& p, const int m0, const int n0,
                                                unsigned char* smem_raw) {
@@ -137,12 +131,7 @@ __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const C
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  const int KT_all = static_cast<int>(ceil_div(p.K, kBK));
-  uint32_t rank = 0;
-  if constexpr (SPLITK == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-  const int kh = (KT_all + 1) / 2;
-  const int kbeg = SPLITK == 2 ? (rank ? kh : 0) : 0;
-  const int KT = SPLITK == 2 ? (rank ? KT_all - kh : kh) : KT_all;  // k-tiles of this CTA, from kbeg
+  const int KT = static_cast<int>(ceil_div(p.K, kBK));
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -158,11 +147,10 @@ __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const C
     const int s = kf % STAGES;
     mbar_expect_tx(full_bar(s), A_BYTES + B_BYTES);
     // outer-contiguous: dims {O, K}, coords {o0, k0}; k-contiguous: {K, O}, {k0, o0}
-    const int kg = kbeg + kf;  // global k-tile
-    if (MC_A) tma_load_2d(stage_a(s), &mapA, m0, kg * kBK, full_bar(s));
-    else tma_load_2d(stage_a(s), &mapA, kg * kBK, m0, full_bar(s));
-    if (MC_B) tma_load_2d(stage_b(s), &mapB, n0, kg * kBK, full_bar(s));
-    else tma_load_2d(stage_b(s), &mapB, kg * kBK, n0, full_bar(s));
+    if (MC_A) tma_load_2d(stage_a(s), &mapA, m0, kf * kBK, full_bar(s));
+    else tma_load_2d(stage_a(s), &mapA, kf * kBK, m0, full_bar(s));
+    if (MC_B) tma_load_2d(stage_b(s), &mapB, n0, kf * kBK, full_bar(s));
+    else tma_load_2d(stage_b(s), &mapB, kf * kBK, n0, full_bar(s));
   };
 
   if (PRODUCER && warp == NCW) {
@@ -171,10 +159,6 @@ __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const C
         if (kf >= STAGES) mbar_wait(empty_bar(kf % STAGES), ((kf / STAGES) + 1) & 1);
         issue(kf);
       }
-    }
-    if constexpr (SPLITK == 2) {  // the producer warp takes part in the cluster barriers
-      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
     }
     return;
   }
@@ -266,44 +250,6 @@ __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const C
     }
   }
 
-  if constexpr (SPLITK == 2) {
-    // rank 1's accumulator -> its own (drained) stage memory -> rank 0 adds it
-    constexpr int NT = NCW * 32;
-    const int ctid = threadIdx.x;
-    if (rank == 1) {
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j)
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            asm volatile("st.shared.f64 [%0], %1;" ::"r"(sbase + (((i * TN + j) * 4 + e) * NT + ctid) * 8),
-                         "d"(acc[i][j][e])
-                         : "memory");
-    }
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-    if (rank == 0) {
-      uint32_t remote;
-      asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(remote) : "r"(sbase));
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            double hi;
-            asm volatile("ld.shared::cluster.f64 %0, [%1];"
-                         : "=d"(hi)
-                         : "r"(remote + (((i * TN + j) * 4 + e) * NT + ctid) * 8)
-                         : "memory");
-            acc[i][j][e] = acc[i][j][e] + hi;
-          }
-    }
-    // rank 1's shared memory stays alive until rank 0 has read it
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-    if (rank == 1) return;
-  }
-
   // Epilogue: C = fma(alpha, acc, beta*C) (beta == 0 never reads C).  Per
   // output row, every C read is issued before the first write, so the reads'
   // latency is paid once per row instead of once per element.
@@ -351,16 +297,15 @@ __device__ __forceinline__ void grouped_tile(int lin, int tiles_m, int tiles_n, 
   tn = in_grp / gsize;
 }
 
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B, int SPLITK = 1>
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B>
 __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32, 1)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, const GemmParams<double> p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   int tm, tn;
-  grouped_tile(static_cast<int>(blockIdx.x) / SPLITK, static_cast<int>(ceil_div(p.M, BM)),
-               static_cast<int>(ceil_div(p.N, BN)), tm, tn);
-  dgemm_tma_tile<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B, SPLITK>(&mapA, &mapB, p, tm * BM, tn * BN,
-                                                                                smem_raw);
+  grouped_tile(static_cast<int>(blockIdx.x), static_cast<int>(ceil_div(p.M, BM)), static_cast<int>(ceil_div(p.N, BN)),
+               tm, tn);
+  dgemm_tma_tile<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B>(&mapA, &mapB, p, tm * BM, tn * BN, smem_raw);
 }
 
 // Wave-tail split: the columns [0, n_main) in 64x64 tiles -- a whole number

@@ -15,35 +15,14 @@ struct Config {
     CUtensorMap ma, mb;
     if (!encode_operand(&ma, p.A, p.lda, p.M, p.K, BM, MC_A)) return false;
     if (!encode_operand(&mb, p.B, p.ldb, p.N, p.K, BN, MC_B)) return false;
+    auto kern = dgemm_tma_kernel<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B>;
     constexpr int slot_a = ((MC_A ? BM + 4 : BM) * kBK * 8 + 1023) / 1024 * 1024;
     constexpr int slot_b = ((MC_B ? BN + 4 : BN) * kBK * 8 + 1023) / 1024 * 1024;
     constexpr int smem = STAGES * (slot_a + slot_b) + 16 * STAGES + 1024;
-    static_assert(STAGES * (slot_a + slot_b) >= (WARPS_M * WARPS_N * 32) * (BM / WARPS_M) * (BN / WARPS_N) / 32 * 8,
-                  "split-K hand-off must fit the stage memory");
-    const unsigned tiles = static_cast<unsigned>(ceil_div(p.M, BM) * ceil_div(p.N, BN));
-    constexpr int threads = (WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32;
-    if (p.split_k == 2 && PRODUCER) {  // 2-CTA cluster per tile, k split between them
-      auto kern = dgemm_tma_kernel<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B, 2>;
-      set_smem(kern, smem);
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(2 * tiles);
-      cfg.blockDim = dim3(threads);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = s;
-      cudaLaunchAttribute attr;
-      attr.id = cudaLaunchAttributeClusterDimension;
-      attr.val.clusterDim.x = 2;
-      attr.val.clusterDim.y = 1;
-      attr.val.clusterDim.z = 1;
-      cfg.attrs = &attr;
-      cfg.numAttrs = 1;
-      if (cudaLaunchKernelEx(&cfg, kern, ma, mb, p) != cudaSuccess) return false;
-      ++launch_counter();
-      return true;
-    }
-    auto kern = dgemm_tma_kernel<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B>;
     set_smem(kern, smem);
-    kern<<<tiles, threads, smem, s>>>(ma, mb, p);
+    const unsigned grid = static_cast<unsigned>(ceil_div(p.M, BM) * ceil_div(p.N, BN));
+    constexpr int threads = (WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32;
+    kern<<<grid, threads, smem, s>>>(ma, mb, p);
     ++launch_counter();
     return true;
   }

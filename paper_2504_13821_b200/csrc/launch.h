@@ -25,10 +25,6 @@ struct GemmParams {
   // Scheduling hint (never changes a bit): 1 when other work runs beside this
   // update (TRMM's concurrent halves), so it keeps the large tiles.
   int busy_gpu = 0;
-  // 2: split K between the two CTAs of a cluster (fp64 TMA path) -- a
-  // different, fixed summation (low half + high half), so it is set for whole
-  // latency-bound calls only, never per update.
-  int split_k = 0;
 };
 
 // Leaf (base-kernel) problem in the reference's Left form on a virtual lower

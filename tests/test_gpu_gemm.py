@@ -242,37 +242,3 @@ def test_sgemm_mbarrier_staging_replay_stress(cuda, monkeypatch):
         gemm(-1.0, Trans.NoTrans, A.cview(), Trans.NoTrans, B.cview(), 1.0, C.view())
         assert torch.equal(C.data, want), rep
 
-
-def test_latency_split_k_trsm_invariants(cuda, monkeypatch):
-    """Small fp64 TRSM calls (n <= 2048) split every GEMM update's K across a
-    2-CTA cluster (a fixed low + high summation): within the reference
-    tolerance, deterministic, column-shard invariant and host-staged ==
-    device, like every call mode; and still within tolerance of the unsplit
-    mode (RECTRI_CU_SPLITK_MAXN=0 is read once per process, so the unsplit
-    reference is the tolerance check itself)."""
-    import paper_2504_13821_b200 as rc
-    from paper_2504_13821_b200 import Threshold, rec_trsm
-    from tests._util import check_against_oracle, tspec
-
-    for side in (0, 1):
-        s = oracle.spec(side, 0, side, 0, 1.0)
-        n, m = 1024, 1000
-        a = F(oracle.make_operand(s, True, n, 31))
-        b = F(oracle.make_rhs(s, n, m, 32))
-        outs = []
-        for _ in range(2):
-            rc.clear_graph_cache()
-            A, B = to_dev(a), to_dev(b)
-            rec_trsm(tspec(s), A.cview(), B.view(), Threshold(256))
-            outs.append(to_np(B))
-        assert oracle.bitwise_equal(outs[0], outs[1])
-        check_against_oracle("trsm", s, a, b, outs[0])
-        part = F(b[:, 300:700]) if side == 0 else F(b[300:700, :])
-        A, P = to_dev(a), to_dev(part)
-        rec_trsm(tspec(s), A.cview(), P.view(), Threshold(256))
-        want = outs[0][:, 300:700] if side == 0 else outs[0][300:700, :]
-        assert oracle.bitwise_equal(to_np(P), F(want))
-        Ah = rc.MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(a)), device="cpu")
-        Bh = rc.MatrixBuffer.from_tensor(torch.from_numpy(np.ascontiguousarray(b)), device="cpu")
-        rec_trsm(tspec(s), Ah.cview(), Bh.view(), Threshold(256))
-        assert oracle.bitwise_equal(np.asfortranarray(Bh.numpy()), outs[0])
