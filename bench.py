@@ -534,7 +534,7 @@ def main():
         B32 = MatrixBuffer(n, m, torch.float32, dev)
         v32, ms32, l32, clk32 = timed("trsm", A32, B32, B32_0)
         fp32 = {"value": v32, "unit": "GFLOP/s", "ms_per_step": ms32, "gpu_launches": l32, "clocks": clk32,
-                "pct_of_ffma_peak": v32 / 1e3 / rc.probe_peak("f32") * 100,
+                "pct_of_ffma2_peak": v32 / 1e3 / rc.probe_peak("f32") * 100,
                 "workload": f"TRSM Left/Lower/NoTrans/NonUnit fp32 n={n}, m={m} per GPU (FFMA path)"}
         if not args.no_cublas and world == 1:
             try:
