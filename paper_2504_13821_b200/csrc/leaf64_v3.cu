@@ -376,15 +376,22 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
         });
       named_sync(1, kThreads);  // X_I visible; cbuf free
     } else {
-      // c += L'_II * b_I; every warp reads b_I before anyone overwrites it
+      // c += L'_II * b_I, and X_I straight to global memory: the panel stays
+      // pristine (the row blocks of a TRMM are independent), so no barrier
+      // between row blocks and no write-back pass
       block_mma(panel_u32 + static_cast<uint32_t>(I * kRB * kNC * 8));
-      named_sync(1, kThreads);
       if (computes)
         for_c([&](int i, int e, int h) {
-          panel[panel_idx<NC>(r0 + crow(i), ccol(e, h))] = p.alpha * csum(i, e, h);
+          const int r = r0 + crow(i), cc = ccol(e, h);
+          if (r < n && cc < ncols) {
+            const i64 sr = p.reflected ? n - 1 - r : r;
+            double* gp = p.right ? p.B + sr * p.ldb + c0 + cc : p.B + (c0 + cc) * p.ldb + sr;
+            *gp = p.alpha * csum(i, e, h);
+          }
         });
     }
   }
+  if (!trsm) return;
   named_sync(1, kThreads);
   for_panel([&](int r, int cc, const double* gp) {
     if (r < n && cc < ncols) *const_cast<double*>(gp) = panel[panel_idx<NC>(r, cc)];
