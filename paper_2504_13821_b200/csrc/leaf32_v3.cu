@@ -317,17 +317,28 @@ __global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams
       }
       named_sync(1, kThreads);  // X_I visible; cbuf free
     } else {
-      block_mma(pcol[0] + I * kRB, pcol[1] + I * kRB);  // + L'_II * b_I
-      named_sync(1, kThreads);                         // every warp has read b_I
+      // + L'_II * b_I, then X_I straight to global memory: later (lower)
+      // row blocks read only panel blocks J < I, so b_I stays intact in
+      // shared memory and no barrier is needed per row block
+      block_mma(pcol[0] + I * kRB, pcol[1] + I * kRB);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
+        const int c = cc + j * kCP;
+        if (c >= ncols) continue;
         float v[4];
         unpack(j, v);
-        *reinterpret_cast<float4*>(pcol[j] + r0 + rw) =
-            make_float4(p.alpha * v[0], p.alpha * v[1], p.alpha * v[2], p.alpha * v[3]);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int r = r0 + rw + t;
+          if (r >= n) break;
+          const i64 sr = p.reflected ? n - 1 - r : r;
+          float* gp = p.right ? p.B + sr * p.ldb + c0 + c : p.B + (c0 + c) * p.ldb + sr;
+          *gp = p.alpha * v[t];
+        }
       }
     }
   }
+  if (!trsm) return;
   named_sync(1, kThreads);
   for_panel([&](int r, int c, const float* g) {
     if (r < n && c < ncols) *const_cast<float*>(g) = panel[c * kPS + r];
