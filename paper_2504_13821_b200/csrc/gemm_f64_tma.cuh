@@ -206,6 +206,7 @@ __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const C
     }
   };
 
+  const uint32_t zero = static_cast<uint32_t>(p.K >> 40);  // 0 at run time, unknown to ptxas
   double acc[TM][TN][4];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
@@ -242,10 +243,15 @@ __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const C
 #pragma unroll
         for (int j = 0; j < TN; ++j) dmma1684(acc[i][j], af[cb][i][0], af[cb][i][1], bf[cb][j]);
       if (kk == 3) {
-        // The last MMAs of the tile have consumed every fragment read from
-        // stage s (so those shared loads are complete): release the stage.
+        // Release stage s once its last fragment loads (this k-step's) have
+        // landed: the arrive's address depends on them (slot_dep, common.cuh).
+        uint32_t dep = 0;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) dep |= slot_dep(zero, af[cb][i][0], af[cb][i][1]);
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dep |= slot_dep(zero, bf[cb][j]);
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty_bar(s));
+        if (lane == 0) mbar_arrive(empty_bar(s) + dep);
       }
     }
   }

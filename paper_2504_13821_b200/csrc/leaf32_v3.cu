@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams
   const int rw = 4 * (tq / kCP), cc = tq % kCP;
   unsigned long long acc[2][2];  // [column][row pair]: (4g, 4g+1), (4g+2, 4g+3)
   int s = 0;
+  const uint32_t dep0 = static_cast<uint32_t>(n) >> 16;  // 0 at run time (n <= 256), unknown to ptxas
   // acc[j] += block(s) * src_j (32 consecutive rows of column j)
   auto block_mma = [&](const float* src0, const float* src1) {
     const int slot = s % kRing;
@@ -268,13 +269,12 @@ __global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams
         }
       }
     }
-    // every fragment read from the slot has been consumed by an FFMA2 above;
-    // order those generic-proxy reads before the async-proxy refill
+    // release the slot once its fragment loads have landed: the arrive's
+    // address depends on the accumulators every loaded A value fed
+    // (slot_dep, common.cuh; FFMA2 latency only, no proxy-fence MEMBAR)
+    const uint32_t dep = slot_dep(dep0, acc[0][0], acc[0][1]);
     __syncwarp();
-    if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      mbar_arrive(empty0 + 8 * slot);
-    }
+    if (lane == 0) mbar_arrive(empty0 + 8 * slot + dep);
     ++s;
   };
   auto unpack = [&](int j, float (&v)[4]) {

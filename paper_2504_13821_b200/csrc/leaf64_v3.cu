@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
     for (int q = 0; q < kParts; ++q) c[q][i][e][h] = 0.0;
   };
   int s = 0;
+  const uint32_t dep0 = static_cast<uint32_t>(p.n) >> 16;  // 0 at run time (n <= 256), unknown to ptxas
   auto block_mma = [&](uint32_t bsrc) {
     if (!computes) return;
     const int slot = s % kRing;
@@ -333,13 +334,16 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
       for (int i = 0; i < WM; ++i)
 #pragma unroll
         for (int e = 0; e < E; ++e) dmma884(c[kk % kParts][i][e][0], c[kk % kParts][i][e][1], a[i][kk], bv[kk][e]);
-    // The DMMAs have consumed every fragment loaded from the slot, so those
-    // loads are complete: only now release the slot to the bulk-copy proxy.
+    // Release the slot once all of its fragment loads have landed: the
+    // arrive's address depends on them (slot_dep, common.cuh) -- cheaper than
+    // a proxy fence, whose MEMBAR would also wait for TRMM's global stores.
+    uint32_t dep = 0;
+#pragma unroll
+    for (int i = 0; i < WM; ++i)
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) dep |= slot_dep(dep0, a[i][kk]);
     __syncwarp();
-    if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads before the async refill
-      mbar_arrive(empty0 + 8 * slot);
-    }
+    if (lane == 0) mbar_arrive(empty0 + 8 * slot + dep);
     ++s;
   };
   auto for_c = [&](auto&& f) {

@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, MINB) leaf5_trmm_kernel(const L
         for (int q = 0; q < kParts; ++q) c[q][mt][e][0] = c[q][mt][e][1] = 0.0;
   };
   zero_c();
+  const uint32_t dep0 = static_cast<uint32_t>(n) >> 16;  // 0 at run time (n <= 256), unknown to ptxas
   for (int s = 0; s < nsteps; ++s) {
     const int slot = s % STAGES;
     int I = 0, J = 0;
@@ -219,11 +220,14 @@ __global__ void __launch_bounds__(kCW * 32 + 32, MINB) leaf5_trmm_kernel(const L
             dmma884(c[kk % kParts][mt][e][0], c[kk % kParts][mt][e][1], a[kk & 1][mt], bv[kk & 1][e]);
       }
     }
+    // release the slot once its fragment loads have landed: the arrive's
+    // address depends on accumulators that every A fragment of the block fed
+    // (slot_dep, common.cuh)
+    uint32_t dep = 0;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) dep |= slot_dep(dep0, c[0][mt][0][0], c[1][mt][0][0]);
     __syncwarp();
-    if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads before the async refill
-      mbar_arrive(empty0 + 8 * slot);
-    }
+    if (lane == 0) mbar_arrive(empty0 + 8 * slot + dep);
     if (has && J == I) {  // row block I complete: X_I = alpha * (c0 + c1) straight to global
       const int r0 = I * kRB;
 #pragma unroll
