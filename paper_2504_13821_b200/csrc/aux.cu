@@ -11,6 +11,7 @@ namespace {
 // of the SM count; each CTA walks whole columns so accesses coalesce.
 template <typename T>
 __global__ void scale_kernel(T* B, i64 ld, i64 rows, i64 cols, T alpha) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   const i64 total = rows * cols;
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
@@ -25,6 +26,7 @@ __global__ void scale_kernel(T* B, i64 ld, i64 rows, i64 cols, T alpha) {
 // computed into S with alpha = 1, beta = 0 -- the same single rounding.
 template <typename T>
 __global__ void accumulate_kernel(T* D, i64 ldd, const T* S, i64 rows, i64 cols, T c) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   const i64 total = rows * cols;
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
@@ -36,6 +38,7 @@ __global__ void accumulate_kernel(T* D, i64 ldd, const T* S, i64 rows, i64 cols,
 
 template <typename T>
 __global__ void diag_zero_scan_kernel(const T* A, i64 lda, i64 n, uint8_t* flags) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   for (i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; r < n;
        r += static_cast<i64>(gridDim.x) * blockDim.x)
     flags[r] = A[r + r * lda] == T(0) ? 1 : 0;
@@ -58,7 +61,7 @@ void scale(T* B, i64 ld, i64 rows, i64 cols, T alpha, cudaStream_t s) {
   const i64 total = rows * cols;
   const i64 want = ceil_div(total, 256);
   const unsigned grid = static_cast<unsigned>(want < 8 * sm_count() ? want : 8 * sm_count());
-  scale_kernel<T><<<grid, 256, 0, s>>>(B, ld, rows, cols, alpha);
+  launch_kernel(scale_kernel<T>, grid, 256, 0, s, B, ld, rows, cols, alpha);
   ++launch_counter();
 }
 
@@ -67,7 +70,7 @@ void accumulate(T* D, i64 ldd, const T* S, i64 rows, i64 cols, T c, cudaStream_t
   if (rows <= 0 || cols <= 0) return;
   const i64 want = ceil_div(rows * cols, 256);
   const unsigned grid = static_cast<unsigned>(want < 8 * sm_count() ? want : 8 * sm_count());
-  accumulate_kernel<T><<<grid, 256, 0, s>>>(D, ldd, S, rows, cols, c);
+  launch_kernel(accumulate_kernel<T>, grid, 256, 0, s, D, ldd, S, rows, cols, c);
   ++launch_counter();
 }
 
@@ -75,7 +78,7 @@ template <typename T>
 void scan(const T* A, i64 lda, i64 n, uint8_t* flags, cudaStream_t s) {
   if (n <= 0) return;
   const unsigned grid = static_cast<unsigned>(ceil_div(n, 256) < sm_count() ? ceil_div(n, 256) : sm_count());
-  diag_zero_scan_kernel<T><<<grid, 256, 0, s>>>(A, lda, n, flags);
+  launch_kernel(diag_zero_scan_kernel<T>, grid, 256, 0, s, A, lda, n, flags);
   ++launch_counter();
 }
 
@@ -245,6 +248,14 @@ int smem_carveout_pct() {
     return e ? atoi(e) : static_cast<int>(cudaSharedmemCarveoutMaxShared);
   }();
   return pct;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RECTRI_CU_PDL");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
 }
 
 }  // namespace rectri_cu

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace rectri_cu {
 
 using i64 = int64_t;
@@ -90,6 +92,42 @@ inline void set_smem(Kern kern, int bytes) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   const int pct = smem_carveout_pct();
   if (pct >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  The recursion is a chain of short
+// kernels per right-hand-side stream (leaf -> update -> leaf ...).  Launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization (launch_kernel), a
+// kernel may be set up before its predecessor has fully retired and waits in
+// griddepcontrol.wait until the predecessor has completed and its memory is
+// visible, so part of the launch latency leaves the critical path while the
+// ordering stays the stream's.  Every kernel launched through launch_kernel
+// calls pdl_wait() before touching global memory; without the
+// attribute it is a no-op.  No kernel triggers its dependents early
+// (griddepcontrol.launch_dependents): measured, an early trigger (at kernel
+// start, or after the main loop) parks the next kernel's CTAs on SMs the
+// other right-hand-side stream needs -- TRSM n = 1024 91 -> 101-121 us --
+// while the implicit trigger at completion gains 1-2 % on small problems
+// (TRSM n = 1024 93.1 -> 91.3 us, fp32 TRSM n = 4096 1910 -> 1881 us;
+// profiles/r02_pdl.txt).  RECTRI_CU_PDL=0 launches without the attribute.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                 Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 }  // namespace rectri_cu

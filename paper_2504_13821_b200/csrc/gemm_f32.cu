@@ -141,6 +141,7 @@ struct FFrag {
 template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB>
 __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
     sgemm_ffma_kernel(const GemmParams<float> p) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   constexpr int TX = BN / 8, TY = BM / 8, NT = TX * TY;
   static_assert(TX == 16 && TY == 16, "16 x 16 thread grid");
   constexpr bool A_KC = TA, B_KC = !TB;  // k-contiguous sources
@@ -317,6 +318,7 @@ __device__ __forceinline__ void read_k(const float* s, int t, int k, float (&v)[
 
 template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB, int BK = kBK>
 __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<float> p) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   constexpr int TX = 16, NT = 256;
   static_assert(BM == 128 && BN == 128, "16 x 16 threads of 8 x 8");
   constexpr bool A_KC = TA, B_KC = !TB;
@@ -496,7 +498,7 @@ void launch_cfg2(const GemmParams<float>& p, cudaStream_t s) {
   constexpr int smem = STAGES * BK * (BM + BN + 2 * kPadMC) * static_cast<int>(sizeof(float));
   set_smem(kern, smem);
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
-  kern<<<grid, 256, smem, s>>>(p);
+  launch_kernel(kern, grid, 256, smem, s, p);
   ++launch_counter();
 }
 
@@ -507,7 +509,7 @@ void launch_cfg(const GemmParams<float>& p, cudaStream_t s) {
       STAGES * (FLayout<BM, TA>::ELEMS + FLayout<BN, !TB>::ELEMS) * static_cast<int>(sizeof(float));
   set_smem(kern, smem);
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
-  kern<<<grid, (BM / 8) * (BN / 8), smem, s>>>(p);
+  launch_kernel(kern, grid, (BM / 8) * (BN / 8), smem, s, p);
   ++launch_counter();
 }
 

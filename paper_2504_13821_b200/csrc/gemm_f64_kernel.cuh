@@ -134,6 +134,7 @@ template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TA,
           int MCMODE>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 1)
     dgemm_dmma_kernel(const GemmParams<double> p) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   constexpr int kBK = BK;
   constexpr int NT = WARPS_M * WARPS_N * 32;
   constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
@@ -322,7 +323,7 @@ struct Config {
     constexpr int smem = STAGES * (BM + BN + 2 * pad) * BK * static_cast<int>(sizeof(double));
     set_smem(kern, smem);
     const unsigned grid = static_cast<unsigned>(ceil_div(p.M, BM) * ceil_div(p.N, BN));
-    kern<<<grid, WARPS_M * WARPS_N * 32, smem, s>>>(p);
+    launch_kernel(kern, grid, WARPS_M * WARPS_N * 32, smem, s, p);
     ++launch_counter();
   }
   static void run(const GemmParams<double>& p, bool ta, bool tb, bool vec2, cudaStream_t s) {

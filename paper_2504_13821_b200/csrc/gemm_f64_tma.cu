@@ -111,7 +111,7 @@ bool split_launch(const GemmParams<double>& p, int n_main, cudaStream_t s) {
   const int smem = split_smem<MC_A, MC_B>();
   set_smem(kern, smem);
   const long long grid = ceil_div(p.M, 64) * (n_main / 64) + ceil_div(p.M, 32) * ceil_div(p.N - n_main, 32);
-  kern<<<static_cast<unsigned>(grid), 5 * 32, smem, s>>>(a64, b64, a32, b32, p, n_main);
+  launch_kernel(kern, static_cast<unsigned>(grid), 5 * 32, smem, s, a64, b64, a32, b32, p, n_main);
   ++launch_counter();
   return true;
 }

@@ -307,6 +307,7 @@ template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, b
 __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32, 1)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, const GemmParams<double> p) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   int tm, tn;
   grouped_tile(static_cast<int>(blockIdx.x), static_cast<int>(ceil_div(p.M, BM)), static_cast<int>(ceil_div(p.N, BN)),
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(5 * 32, 1)
     dgemm_tma_split_kernel(const __grid_constant__ CUtensorMap a64, const __grid_constant__ CUtensorMap b64,
                            const __grid_constant__ CUtensorMap a32, const __grid_constant__ CUtensorMap b32,
                            const GemmParams<double> p, const int n_main) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int tiles_m64 = static_cast<int>(ceil_div(p.M, 64));
   const int main_tiles = tiles_m64 * (n_main / 64);

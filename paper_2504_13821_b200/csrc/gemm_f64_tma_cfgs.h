@@ -22,7 +22,7 @@ struct Config {
     set_smem(kern, smem);
     const unsigned grid = static_cast<unsigned>(ceil_div(p.M, BM) * ceil_div(p.N, BN));
     constexpr int threads = (WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32;
-    kern<<<grid, threads, smem, s>>>(ma, mb, p);
+    launch_kernel(kern, grid, threads, smem, s, ma, mb, p);
     ++launch_counter();
     return true;
   }

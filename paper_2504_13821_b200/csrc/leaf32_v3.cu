@@ -100,6 +100,7 @@ __device__ void pack32_block(const LeafParams<float>& p, float* __restrict__ P, 
 }
 
 __global__ void __launch_bounds__(256) pack32_kernel(const LeafParams<float> p, float* __restrict__ P) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   pack32_block(p, P, blockIdx.x);
 }
 
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(256) pack32_kernel(const LeafParams<float> p, 
 __global__ void __launch_bounds__(256) pack32_all_kernel(const LeafParams<float> base, const long long* __restrict__ r0s,
                                                          const int* __restrict__ ns, float* __restrict__ P,
                                                          long long stride) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   const int k = blockIdx.y;
   LeafParams<float> p = base;
   p.n = ns[k];
@@ -155,6 +157,7 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 template <int NC>
 __global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams<float> p,
                                                                 const float* __restrict__ P) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   constexpr int kNC = NC;
   constexpr int kWarps = NC / 8;
   constexpr int kThreads = kWarps * 32;
@@ -352,7 +355,7 @@ void launch_leaf32_pack_all(const LeafParams<float>& base, const long long* d_r0
   using namespace leaf32v3;
   constexpr int kMaxBlk = kLeafMax / kRB;
   dim3 grid(kMaxBlk * (kMaxBlk + 1) / 2, nleaves);
-  pack32_all_kernel<<<grid, 256, 0, s>>>(base, d_r0, d_n, scratch, stride);
+  launch_kernel(pack32_all_kernel, grid, 256, 0, s, base, d_r0, d_n, scratch, stride);
   ++launch_counter();
 }
 
@@ -360,12 +363,12 @@ void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t
   using namespace leaf32v3;
   const int nblk = (p.n + kRB - 1) / kRB;
   if (!prepacked && (p.trsm || p.alpha != 0.f)) {
-    pack32_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, scratch);
+    launch_kernel(pack32_kernel, nblk * (nblk + 1) / 2, 256, 0, s, p, scratch);
     ++launch_counter();
   }
   auto go = [&](auto kern, int width, int smem) {
     set_smem(kern, smem);
-    kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), 4 * width + 32, smem, s>>>(p, scratch);
+    launch_kernel(kern, static_cast<unsigned>(ceil_div(p.nrhs, width)), 4 * width + 32, smem, s, p, scratch);
   };
   const int nc = leaf3_width(p.nrhs, p.trsm != 0);
   if (nc == 32) go(leaf32_kernel<32>, 32, smem_bytes<32>());

@@ -135,6 +135,7 @@ __device__ void pack3_block(const LeafParams<double>& p, double* __restrict__ P,
 }
 
 __global__ void __launch_bounds__(256) pack3_kernel(const LeafParams<double> p, double* __restrict__ P) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   pack3_block(p, P, blockIdx.x);
 }
 
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(256) pack3_kernel(const LeafParams<double> p, 
 __global__ void __launch_bounds__(256) pack3_all_kernel(const LeafParams<double> base, const long long* __restrict__ r0s,
                                                         const int* __restrict__ ns, double* __restrict__ P,
                                                         long long stride) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   const int k = blockIdx.y;
   LeafParams<double> p = base;
   p.n = ns[k];
@@ -204,6 +206,7 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 template <int NC, int WM = 1>
 __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParams<double> p,
                                                                 const double* __restrict__ P) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   constexpr int kNC = NC;
   constexpr int CW = WM == 2 ? 4 : (NC >= 16 ? 8 : 4);  // compute warps
   constexpr int E = 4 * (NC / 8) / CW / WM;              // column tiles per compute warp
@@ -427,14 +430,14 @@ void launch_leaf3_pack_all(const LeafParams<double>& base, const long long* d_r0
                            double* scratch, cudaStream_t s) {
   using namespace leaf64v3;
   dim3 grid(kMaxBlk * (kMaxBlk + 1) / 2, nleaves);
-  pack3_all_kernel<<<grid, 256, 0, s>>>(base, d_r0, d_n, scratch, static_cast<long long>(kScratchDoubles));
+  launch_kernel(pack3_all_kernel, grid, 256, 0, s, base, d_r0, d_n, scratch, static_cast<long long>(kScratchDoubles));
   ++launch_counter();
 }
 
 void launch_leaf3_pack(const LeafParams<double>& p, double* dst, cudaStream_t s) {
   using namespace leaf64v3;
   const int nblk = (p.n + kRB - 1) / kRB;
-  pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(p, dst);
+  launch_kernel(pack3_kernel, nblk * (nblk + 1) / 2, 256, 0, s, p, dst);
   ++launch_counter();
 }
 
@@ -450,7 +453,7 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
   if (!prepacked && !zero) {
     LeafParams<double> q = p;
     q.pack_asc = v5 ? 1 : 0;
-    pack3_kernel<<<nblk * (nblk + 1) / 2, 256, 0, s>>>(q, scratch);
+    launch_kernel(pack3_kernel, nblk * (nblk + 1) / 2, 256, 0, s, q, scratch);
     ++launch_counter();
   }
   if (v5) {
@@ -460,7 +463,7 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
   const int nc = leaf3_width(p.nrhs, p.trsm != 0);
   auto go = [&](auto kern, int width, int smem) {
     set_smem(kern, smem);
-    kern<<<static_cast<unsigned>(ceil_div(p.nrhs, width)), kThreads + 32, smem, s>>>(p, scratch);
+    launch_kernel(kern, static_cast<unsigned>(ceil_div(p.nrhs, width)), kThreads + 32, smem, s, p, scratch);
   };
   const char* wm = getenv("RECTRI_CU_LEAF_WM");
   if (nc == 32 && wm && atoi(wm) == 2) go(leaf3_kernel<32, 2>, 32, smem_bytes<32>());

@@ -100,6 +100,7 @@ constexpr int smem_bytes() { return (kLeafMax * NC + STAGES * kCW * kBlk) * 8 + 
 template <int NC, int STAGES, int MINB>
 __global__ void __launch_bounds__(kCW * 32 + 32, MINB) leaf5_trmm_kernel(const LeafParams<double> p,
                                                                       const double* __restrict__ P) {
+  pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   constexpr int E = NC / 8;  // 8-column tiles per warp
   extern __shared__ __align__(128) double smem5[];
   double* panel = smem5;                   // kLeafMax x NC (swizzled rows)
@@ -250,7 +251,7 @@ void go(const LeafParams<double>& p, const double* P, cudaStream_t s) {
   auto kern = leaf5_trmm_kernel<NC, STAGES, MINB>;
   constexpr int smem = smem_bytes<NC, STAGES>();
   set_smem(kern, smem);
-  kern<<<static_cast<unsigned>(ceil_div(p.nrhs, NC)), kCW * 32 + 32, smem, s>>>(p, P);
+  launch_kernel(kern, static_cast<unsigned>(ceil_div(p.nrhs, NC)), kCW * 32 + 32, smem, s, p, P);
   ++launch_counter();
 }
 
