@@ -1166,6 +1166,8 @@ template <typename T>
 bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, DView<T> hB, i64 threshold,
                        const BackendInfo& be, rectri_cu_event_fn sink, void* user, int dev,
                        PageableStager* pg = nullptr) {
+  const auto entry_t0 = std::chrono::steady_clock::now();
+  std::chrono::steady_clock::time_point tmark[3];  // RECTRI_CU_E2E_TRACE: setup phases
   const bool left = spec.side == RECTRI_CU_LEFT;
   const i64 n = A.rows, brows = hB.rows, bcols = hB.cols;
   const size_t bbytes = static_cast<size_t>(brows * bcols) * sizeof(T);
@@ -1176,14 +1178,21 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
   {
     std::lock_guard<std::mutex> lock(g_mu);
     res = &device_res(dev);
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
+    // Query free memory only when the staging buffers must grow: on a busy
+    // box cudaMemGetInfo took 0.1-72 ms per call (e2e trace), the largest
+    // source of the end-to-end step variance.
     const size_t have = (a_dev ? 0 : res->stage_bytes[0]) + res->stage_bytes[1];
-    const size_t room = free_b + have > (size_t{1} << 30) ? free_b + have - (size_t{1} << 30) : 0;
-    if (abytes + bbytes > room) return false;
+    if (abytes > (a_dev ? 0 : res->stage_bytes[0]) || bbytes > res->stage_bytes[1]) {
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      const size_t room = free_b + have > (size_t{1} << 30) ? free_b + have - (size_t{1} << 30) : 0;
+      if (abytes + bbytes > room) return false;
+    }
+    tmark[0] = std::chrono::steady_clock::now();
     if (!a_dev) dAp = static_cast<T*>(staging(*res, 0, abytes));
     dBp = static_cast<T*>(staging(*res, 1, bbytes));
   }
+  tmark[1] = std::chrono::steady_clock::now();
   const DView<const T> dA = a_dev ? A : DView<const T>{dAp, n, n, n};
   const DView<T> dB{dBp, brows, brows, bcols};
   Spec eff = spec;
@@ -1198,6 +1207,7 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
     dry.kernels = [&](const KDesc<T>& k) { ks.push_back(k); };
     dry.run(eff, dA, dB, 0);
   }
+  tmark[2] = std::chrono::steady_clock::now();
   if (sink)
     for (const Ev& e : evs_logical) sink(user, e.e, e.n, e.m);
 
@@ -1268,8 +1278,12 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
     evs.push_back(e);
     return e;
   };
+  // RECTRI_CU_E2E_NOCOPY=1 (timing experiments only; the result is garbage):
+  // skip every transfer, leaving the streamed path's compute schedule alone.
+  static const bool nocopy = getenv("RECTRI_CU_E2E_NOCOPY") != nullptr;
   auto copy2d = [&](T* dst, i64 dld, const T* src, i64 sld, i64 rows, i64 cols, cudaMemcpyKind kind,
                     cudaStream_t st) {
+    if (nocopy) return;
     if (pg && kind == cudaMemcpyHostToDevice && pg->covers(src)) {  // pageable source: pinned bounce
       pg->h2d(dst, sizeof(T) * dld, src, sizeof(T) * sld, sizeof(T) * rows, cols, st);
       return;
@@ -1460,7 +1474,16 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
     cuda_check(cudaStreamSynchronize(hs), "synchronize");
     if (pg) pg->finish();  // pageable B: the copy-backs into user memory
     if (trace) {
-      fprintf(stderr, "e2e trace: host enqueue %.2f ms\n", host_ms);
+      auto ms_since = [](std::chrono::steady_clock::time_point a) {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+      };
+      auto ms_between = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+      };
+      fprintf(stderr, "e2e trace: entry -> start %.2f ms (meminfo %.2f, staging %.2f, descriptor run %.2f), "
+              "host enqueue %.2f ms, entry -> synced %.2f ms\n",
+              ms_since(entry_t0) - ms_since(host_t0), ms_between(entry_t0, tmark[0]), ms_between(tmark[0], tmark[1]),
+              ms_between(tmark[1], tmark[2]), host_ms, ms_since(entry_t0));
       float t[3] = {0, 0, 0};
       for (int q = 0; q < 3; ++q) cudaEventElapsedTime(&t[q], start, t_end[q]);
       fprintf(stderr, "e2e trace: h2d done %.2f ms, compute done %.2f ms, d2h done %.2f ms, %zu units, %d chunks\n",
@@ -1496,6 +1519,9 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
           f.index = r;
           throw f;
         }
+  if (trace)
+    fprintf(stderr, "e2e trace: entry -> return %.2f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - entry_t0).count());
   return true;
 }
 
