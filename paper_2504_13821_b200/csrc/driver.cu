@@ -1322,7 +1322,17 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
     const i64 rhs = left ? bcols : brows;
     int TP = static_cast<int>(std::max<i64>(1, std::min<i64>(16, rhs / 8192)));
     if (const char* te = getenv("RECTRI_CU_E2E_PANELS")) TP = std::max(1, atoi(te));
-    const i64 tw = (rhs + TP - 1) / TP;
+    // Panel boundaries: TP equal panels, or (RECTRI_CU_E2E_FIRST, tuning)
+    // a first panel of that width and TP - 1 equal ones after it.
+    std::vector<i64> tb{0};
+    {
+      const char* fe = getenv("RECTRI_CU_E2E_FIRST");
+      const i64 first = fe && TP > 1 ? std::min<i64>(rhs, (atoll(fe) + 63) / 64 * 64) : 0;
+      if (first > 0) tb.push_back(first);
+      const int rest = first > 0 ? TP - 1 : TP;
+      const i64 w = (rhs - tb.back() + rest - 1) / rest;
+      while (tb.back() < rhs) tb.push_back(std::min(rhs, tb.back() + w));
+    }
     auto window = [&](DView<T> v, i64 r0, i64 r1) {
       return left ? v.sub(0, r0, v.rows, r1 - r0) : v.sub(r0, 0, r1 - r0, v.cols);
     };
@@ -1338,8 +1348,8 @@ bool run_host_streamed(OpK op, const Spec& spec, DView<const T> A, bool a_dev, D
     std::vector<cudaEvent_t> packed_evs(units.size(), nullptr);
     // TRMM triangles in the v4 / v5 leaves' ascending order
     const int pack_asc = pack_once && op == kTrmm && leaf_trmm_asc() ? 1 : 0;
-    for (int tp = 0; tp < TP && tp * tw < rhs; ++tp) {
-      const i64 t0 = tp * tw, t1 = std::min(rhs, t0 + tw);
+    for (int tp = 0; tp + 1 < static_cast<int>(tb.size()); ++tp) {
+      const i64 t0 = tb[tp], t1 = tb[tp + 1];
       // H2D in first-use order (A blocks in the first panel); ready[i] gates unit i.
       std::vector<cudaEvent_t> ready(units.size(), nullptr);
       std::vector<std::vector<int>> fresh(units.size());  // chunks first loaded for unit i

@@ -28,7 +28,9 @@
 // scratch straight into registers one block ahead.  Per row block: GEMM
 // part, (TRSM) the negated partial result to shared memory + barrier, the
 // diagonal-block product, store + barrier.
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "launch.h"
@@ -85,24 +87,36 @@ __device__ void pack3_block(const LeafParams<double>& p, double* __restrict__ P,
   const int r0 = I * kRB, j0 = J * kRB;
   double* dst = P + static_cast<size_t>(seq_of(I, J, nblk, trsm || p.pack_asc)) * kBlk;
   const int tid = threadIdx.x;
+  // 256 threads, 4 elements each: every load of a thread is issued before
+  // its first store, so the A reads' latency is paid once, not four times
+  // (the stores to P could alias A as far as the compiler knows).
+  constexpr int kPer = kBlk / 256;
+  double v[kPer];
   if (J < I) {
-    for (int o = tid; o < kBlk; o += blockDim.x) {
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int o = tid + 256 * e;
       const int ln = o & 31, kk = (o >> 5) & 7, mt = o >> 8;
       const int r = 8 * mt + (ln >> 2), k = 4 * kk + (ln & 3);
-      dst[o] = r0 + r < p.n ? lprime(p, r0 + r, j0 + k) : 0.0;
+      v[e] = r0 + r < p.n ? lprime(p, r0 + r, j0 + k) : 0.0;
     }
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) dst[tid + 256 * e] = v[e];
     return;
   }
   // diagonal block: lower triangle with its diagonal (1 for Unit; identity
   // on padding rows), zeros above
-  for (int o = tid; o < kBlk; o += blockDim.x) {
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const int o = tid + 256 * e;
     const int r = o >> 5, k = o & 31;
-    double v = 0.0;
-    if (r0 + r >= p.n) v = r == k ? 1.0 : 0.0;
-    else if (k < r) v = lprime(p, r0 + r, r0 + k);
-    else if (k == r) v = p.unit ? 1.0 : lprime(p, r0 + r, r0 + r);
-    L[r][k] = v;
+    v[e] = 0.0;
+    if (r0 + r >= p.n) v[e] = r == k ? 1.0 : 0.0;
+    else if (k < r) v[e] = lprime(p, r0 + r, r0 + k);
+    else if (k == r) v[e] = p.unit ? 1.0 : lprime(p, r0 + r, r0 + r);
   }
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) L[(tid + 256 * e) >> 5][(tid + 256 * e) & 31] = v[e];
   __syncthreads();
   if (!trsm) {
     for (int o = tid; o < kBlk; o += blockDim.x) {
@@ -255,6 +269,10 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
       });
     return;
   }
+  // RECTRI_CU_LEAF_TRACE (direct base calls, diagnostics): clock64 stamps of
+  // thread 0 -- start, panel loaded, each row block done, write-back done.
+  long long* tr = p.trace && tid == 0 ? p.trace + static_cast<size_t>(blockIdx.x) * 48 : nullptr;
+  if (tr) tr[0] = clock64();
   const int nseq = nblk * (nblk + 1) / 2;
   if (tid == 0) {
     for (int q = 0; q < kRing; ++q) {
@@ -292,6 +310,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
   const uint32_t a_off = static_cast<uint32_t>((mt0 * 8 * 32 + lane) * 8);  // k-step-0 A fragment, row tile mt0
   cp_async_wait<0>();
   named_sync(1, kThreads);  // panel loaded (GEMM warps only; the producer runs free)
+  if (tr) tr[1] = clock64();
   if (trsm && p.alpha != 1.0) {  // x = alpha * b (base_kernels.cpp:76-77)
     for_panel([&](int r, int c, const double*) { panel[panel_idx<NC>(r, c)] *= p.alpha; });
     named_sync(1, kThreads);
@@ -299,6 +318,10 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
   // element (i, e, h) of this lane's accumulators: row 8(mt0+i)+g, column 8(nt0+e)+2t+h of the row block
   auto crow = [&](int i) { return 8 * (mt0 + i) + g; };
   auto ccol = [&](int e, int h) { return 8 * (nt0 + e) + 2 * t + h; };
+  auto gaddr = [&](int r, int cc) -> double* {  // B element of panel row r, column cc
+    const i64 sr = p.reflected ? n - 1 - r : r;
+    return p.right ? p.B + sr * p.ldb + c0 + cc : p.B + (c0 + cc) * p.ldb + sr;
+  };
 
   // c[q][i][e][h] += A(block s) * Bsrc(32 rows at byte offset bsrc of a
   // row-major [k][kNC] swizzled buffer), k-step kk into partial sum
@@ -390,19 +413,17 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
       if (computes)
         for_c([&](int i, int e, int h) {
           const int r = r0 + crow(i), cc = ccol(e, h);
-          if (r < n && cc < ncols) {
-            const i64 sr = p.reflected ? n - 1 - r : r;
-            double* gp = p.right ? p.B + sr * p.ldb + c0 + cc : p.B + (c0 + cc) * p.ldb + sr;
-            *gp = p.alpha * csum(i, e, h);
-          }
+          if (r < n && cc < ncols) *gaddr(r, cc) = p.alpha * csum(i, e, h);
         });
     }
+    if (tr) tr[2 + bi] = clock64();
   }
   if (!trsm) return;
   named_sync(1, kThreads);
   for_panel([&](int r, int cc, const double* gp) {
     if (r < n && cc < ncols) *const_cast<double*>(gp) = panel[panel_idx<NC>(r, cc)];
   });
+  if (tr) tr[41] = clock64();
 }
 
 }  // namespace leaf64v3
@@ -461,9 +482,18 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
     return;
   }
   const int nc = leaf3_width(p.nrhs, p.trsm != 0);
+  const char* trv = getenv("RECTRI_CU_LEAF_TRACE");
+  LeafParams<double> q = p;
+  long long* d_tr = nullptr;
+  const unsigned grid = static_cast<unsigned>(ceil_div(p.nrhs, nc));
+  if (trv && atoi(trv) && !prepacked) {
+    cudaMalloc(&d_tr, grid * 48 * sizeof(long long));
+    cudaMemset(d_tr, 0, grid * 48 * sizeof(long long));
+    q.trace = d_tr;
+  }
   auto go = [&](auto kern, int width, int smem) {
     set_smem(kern, smem);
-    launch_kernel(kern, static_cast<unsigned>(ceil_div(p.nrhs, width)), kThreads + 32, smem, s, p, scratch);
+    launch_kernel(kern, static_cast<unsigned>(ceil_div(p.nrhs, width)), kThreads + 32, smem, s, q, scratch);
   };
   const char* wm = getenv("RECTRI_CU_LEAF_WM");
   if (nc == 32 && wm && atoi(wm) == 2) go(leaf3_kernel<32, 2>, 32, smem_bytes<32>());
@@ -471,6 +501,19 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
   else if (nc == 16) go(leaf3_kernel<16>, 16, smem_bytes<16>());
   else go(leaf3_kernel<8>, 8, smem_bytes<8>());
   ++launch_counter();
+  if (d_tr) {  // diagnostics: mean cycles from CTA start per phase, on stderr
+    cudaStreamSynchronize(s);
+    std::vector<long long> h(grid * 48);
+    cudaMemcpy(h.data(), d_tr, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaFree(d_tr);
+    double acc[48] = {0};
+    for (unsigned b = 0; b < grid; ++b)
+      for (int k = 1; k < 48; ++k)
+        if (h[b * 48 + k]) acc[k] += static_cast<double>(h[b * 48 + k] - h[b * 48]);
+    fprintf(stderr, "leaf3 trace (NC %d, %u CTAs, mean cycles from CTA start): panel %.0f |", nc, grid, acc[1] / grid);
+    for (int bi = 0; bi < nblk; ++bi) fprintf(stderr, " %.0f", acc[2 + bi] / grid);
+    fprintf(stderr, " | end %.0f\n", acc[41] / grid);
+  }
 }
 
 }  // namespace rectri_cu
