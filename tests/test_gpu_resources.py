@@ -195,3 +195,45 @@ def test_pageable_host_operands_singular_and_exact(cuda):
     with pytest.raises(SingularityError) as e:
         rec_trsm(tspec(s), A2.cview(), B2.view(), Threshold(256), Backend.cuda(device=0))
     assert e.value.index() == 777
+
+
+_PDL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import oracle
+import paper_2504_13821_b200 as rc
+from paper_2504_13821_b200 import Backend, Threshold, rec_trmm, rec_trsm
+from tests._util import to_dev, to_np, tspec
+outs = []
+for dt in (np.float64, np.float32):
+    for op, uplo in (("trsm", 0), ("trmm", 1)):
+        s = oracle.spec(0, uplo, 0, 0, 1.0)
+        a = oracle.make_dominant(1024, uplo, 5).astype(dt)
+        b = oracle.make_random(1024, 1500, 6).astype(dt)
+        A, B = to_dev(np.asfortranarray(a)), to_dev(np.asfortranarray(b))
+        (rec_trsm if op == "trsm" else rec_trmm)(tspec(s), A.cview(), B.view(), Threshold(256), Backend.cuda())
+        outs.append(to_np(B))
+np.savez({out!r}, *outs)
+"""
+
+
+def test_pdl_launch_is_bitwise_neutral(cuda, tmp_path):
+    """Programmatic dependent launch (RECTRI_CU_PDL, read once per process)
+    only moves launch latency: captured recursions give the same bits with
+    and without it, both precisions, TRSM and TRMM."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    res = []
+    for pdl in ("0", "1"):
+        out = str(tmp_path / f"pdl{pdl}.npz")
+        env = dict(os.environ, RECTRI_CU_PDL=pdl)
+        r = subprocess.run([sys.executable, "-c", _PDL_SCRIPT.format(root=root, out=out)], env=env,
+                           capture_output=True, text=True, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        z = np.load(out)
+        res.append([z[k] for k in sorted(z.files)])
+    for x, y in zip(*res):
+        assert oracle.bitwise_equal(x, y)
