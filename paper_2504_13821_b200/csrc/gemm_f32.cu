@@ -307,20 +307,31 @@ struct TLoaderKC {
   }
 };
 
-template <int BO>
-__device__ __forceinline__ void read_k(const float* s, int t, int k, float (&v)[8]) {
-  constexpr int RS = BO + kPadMC;
-  const float4 a = *reinterpret_cast<const float4*>(s + k * RS + 4 * t);
-  const float4 b = *reinterpret_cast<const float4*>(s + k * RS + BO / 2 + 4 * t);
-  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+// Thread t's CN values of k-step k: CN / 4 float4 runs, at 4t + q * BO / (CN / 4).
+template <int BO, int CN = 8>
+__device__ __forceinline__ void read_k(const float* s, int t, int k, float (&v)[CN]) {
+  constexpr int RS = BO + kPadMC, Q = CN / 4;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const float4 a = *reinterpret_cast<const float4*>(s + k * RS + q * (BO / Q) + 4 * t);
+    v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+  }
 }
+// Outer index (row of A / column of B within the tile) of value j of thread t.
+template <int BO, int CN = 8>
+__device__ __forceinline__ int outer_k(int t, int j) { return (j / 4) * (BO / (CN / 4)) + 4 * t + (j & 3); }
 
+// BN = 128: 16 x 16 threads of 8 x 8 (two CTAs per SM); BN = 256: 8 x 16
+// per thread (one CTA per SM): per k-step a warp issues 6 LDS.128 for 64
+// FFMA2 instead of 4 for 32 -- the shared-memory wavefronts, not the FMA
+// pipe, bound the 8 x 8 tile (ncu: 76 % of shared bandwidth at 85 % FMA).
+// Same k-ascending chain per element either way: bitwise equal.
 template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB, int BK = kBK>
-__global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<float> p) {
+__global__ void __launch_bounds__(256, BN == 128 ? 2 : 1) sgemm_ffma2_kernel(const GemmParams<float> p) {
   pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   constexpr int TX = 16, NT = 256;
-  static_assert(BM == 128 && BN == 128, "16 x 16 threads of 8 x 8");
+  constexpr int CN = BN / 16;  // columns per thread
+  static_assert(BM == 128 && (BN == 128 || BN == 256), "16 x 16 threads of 8 x CN");
   constexpr bool A_KC = TA, B_KC = !TB;
   constexpr int A_EL = BK * (BM + kPadMC), B_EL = BK * (BN + kPadMC);
   using LA = std::conditional_t<A_KC, TLoaderKC<BM, NT, BK>, FLoader<BM, NT, VA, false, BK>>;
@@ -338,11 +349,11 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
   la.init(p.A, p.lda, m0, p.M, p.K);
   lb.init(p.B, p.ldb, n0, p.N, p.K);
 
-  unsigned long long acc2[4][8];
+  unsigned long long acc2[4][CN];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc2[i][j] = 0ull;
+    for (int j = 0; j < CN; ++j) acc2[i][j] = 0ull;
 
   // Stage s holds k-tile j with j % STAGES == s.  full[s]: every thread's
   // cp.async copies of the tile have landed (cp.async.mbarrier.arrive.noinc,
@@ -382,11 +393,12 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
 #pragma unroll
   for (int s = 0; s < STAGES; ++s)
     if (s < KT) fill(s, s);
-  float fa[2][8], fb[2][8];
+  float fa[2][8], fb[2][CN];
   bar_wait(full0, 0);
   read_k<BM>(sA, ty, 0, fa[0]);
-  read_k<BN>(sB, tx, 0, fb[0]);
+  read_k<BN, CN>(sB, tx, 0, fb[0]);
   int st = 0;
+  const uint32_t dep0 = static_cast<uint32_t>(p.K >> 40);  // 0 at run time, unknown to ptxas
   for (i64 kt = 0; kt < KT; ++kt) {
     const int cur = st;
     const float* a_s = sA + st * A_EL;
@@ -396,7 +408,7 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
       const int cb = k & 1;
       if (k + 1 < BK) {
         read_k<BM>(a_s, ty, k + 1, fa[cb ^ 1]);
-        read_k<BN>(b_s, tx, k + 1, fb[cb ^ 1]);
+        read_k<BN, CN>(b_s, tx, k + 1, fb[cb ^ 1]);
       } else {
         // refill the stage of tile kt - 1 (released after its last FFMAs) with tile kt + STAGES - 1
         const i64 nt = kt + STAGES - 1;
@@ -409,7 +421,7 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
         if (kt + 1 < KT) {
           bar_wait(full0 + 8 * st, static_cast<uint32_t>(((kt + 1) / STAGES) & 1));
           read_k<BM>(sA + st * A_EL, ty, 0, fa[cb ^ 1]);
-          read_k<BN>(sB + st * B_EL, tx, 0, fb[cb ^ 1]);
+          read_k<BN, CN>(sB + st * B_EL, tx, 0, fb[cb ^ 1]);
         }
       }
 #pragma unroll
@@ -417,18 +429,25 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
         unsigned long long ap;
         asm("mov.b64 %0, {%1, %2};" : "=l"(ap) : "f"(fa[cb][2 * ip]), "f"(fa[cb][2 * ip + 1]));
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < CN; ++j) {
           unsigned long long bb;
           asm("mov.b64 %0, {%1, %1};" : "=l"(bb) : "f"(fb[cb][j]));
           asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[ip][j]) : "l"(ap), "l"(bb));
         }
       }
     }
-    // this warp's last reads of tile kt have been consumed by the FFMAs above
-    // (so they are complete): release the stage
+    // release the stage once this warp's last reads of tile kt have landed:
+    // the arrive's address depends on accumulators every one of those
+    // fragments fed (slot_dep, common.cuh: ptxas may otherwise issue the
+    // arrive while the loads are in flight)
+    uint32_t dep = 0;
+#pragma unroll
+    for (int ip = 0; ip < 4; ++ip) dep |= slot_dep(dep0, acc2[ip][0]);
+#pragma unroll
+    for (int j = 1; j < CN; ++j) dep |= slot_dep(dep0, acc2[0][j]);
     __syncwarp();
     if ((threadIdx.x & 31) == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(empty0 + 8 * cur) : "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(empty0 + 8 * cur + dep) : "memory");
   }
   cp_async_wait<0>();
 
@@ -440,11 +459,11 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
   const bool vec = m0 + BM <= p.M && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && p.ldc % 4 == 0;
   if (vec) {
 #pragma unroll
-    for (int jb = 0; jb < 8; jb += 4) {
+    for (int jb = 0; jb < CN; jb += 4) {
       float4 cv[4][2];
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
-        const i64 n = n0 + FFrag<BN, false>::outer(tx, jb + jj);
+        const i64 n = n0 + outer_k<BN, CN>(tx, jb + jj);
         const float* cp = p.C + m0 + 4 * ty + n * p.ldc;
         const bool rd = !beta_zero && n < p.N;
         cv[jj][0] = rd ? *reinterpret_cast<const float4*>(cp) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -453,7 +472,7 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
         const int j = jb + jj;
-        const i64 n = n0 + FFrag<BN, false>::outer(tx, j);
+        const i64 n = n0 + outer_k<BN, CN>(tx, j);
         if (n >= p.N) continue;
         float a[8];
 #pragma unroll
@@ -472,8 +491,8 @@ __global__ void __launch_bounds__(256, 2) sgemm_ffma2_kernel(const GemmParams<fl
     return;
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const i64 n = n0 + FFrag<BN, false>::outer(tx, j);
+  for (int j = 0; j < CN; ++j) {
+    const i64 n = n0 + outer_k<BN, CN>(tx, j);
     if (n >= p.N) continue;
     float accj[8], cold[8];
 #pragma unroll
@@ -576,7 +595,17 @@ void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t 
   const char* e = getenv("RECTRI_CU_SGEMM_BK");
   const int forced = e ? atoi(e) : 0;
   const int bk = forced == 16 || forced == 32 ? forced : (ta ? 16 : 32);
-  if (sgemm_version() == 2 && bk == 32) dispatch2<128, 128, 3, 32>(p, ta, tb, s);
+  // 128 x 256 tiles (8 x 16 per thread, one CTA per SM) for updates with at
+  // least four waves of them: +3-8 % on the long updates (fewer shared
+  // wavefronts per FMA), but a quarter of the 128 x 128 CTAs per SM slot
+  // would starve the short ones (fp32 TRSM n = 4096 1925 -> 2105 us if
+  // forced).  RECTRI_CU_SGEMM_WIDE = 0 / 1 forces it off / on.
+  const char* w = getenv("RECTRI_CU_SGEMM_WIDE");
+  const i64 wide_tiles = ceil_div(p.M, 128) * ceil_div(p.N, 256);
+  const bool wide = w ? atoi(w) == 1 : wide_tiles >= 4 * 148;
+  if (sgemm_version() == 2 && wide && bk == 32) dispatch2<128, 256, 3, 32>(p, ta, tb, s);
+  else if (sgemm_version() == 2 && wide) dispatch2<128, 256, 3>(p, ta, tb, s);
+  else if (sgemm_version() == 2 && bk == 32) dispatch2<128, 128, 3, 32>(p, ta, tb, s);
   else if (sgemm_version() == 2) dispatch2<128, 128, 3>(p, ta, tb, s);
   else dispatch<128, 128, 3>(p, ta, tb, s);
 }

@@ -158,14 +158,16 @@ def test_sgemm_v2_bitwise_equals_v1(cuda, ta, tb, monkeypatch):
             av = A.cview().subview(off, 2, K, M) if ta else A.cview().subview(off, 2, M, K)
             bv = B.cview().subview(off, 2, N, K) if tb else B.cview().subview(off, 2, K, N)
             outs = []
-            for ver, bk in (("1", "16"), ("2", "16"), ("2", "32")):
+            variants = (("1", "16", "0"), ("2", "16", "0"), ("2", "32", "0"), ("2", "16", "1"), ("2", "32", "1"))
+            for ver, bk, wide in variants:
                 monkeypatch.setenv("RECTRI_CU_SGEMM", ver)
                 monkeypatch.setenv("RECTRI_CU_SGEMM_BK", bk)
+                monkeypatch.setenv("RECTRI_CU_SGEMM_WIDE", wide)  # 128x256 tiles, 8x16 per thread
                 C = to_dev(c0)
                 gemm(alpha, Trans(ta), av, Trans(tb), bv, beta, C.view().subview(2, 0, M, N))
                 outs.append(to_np(C))
-            assert oracle.bitwise_equal(outs[0], outs[1]), (M, N, K, off, alpha, beta)
-            assert oracle.bitwise_equal(outs[0], outs[2]), (M, N, K, off, alpha, beta, "bk32")
+            for o, v in zip(outs[1:], variants[1:]):
+                assert oracle.bitwise_equal(outs[0], o), (M, N, K, off, alpha, beta, v)
 
 
 @pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
@@ -237,8 +239,10 @@ def test_sgemm_mbarrier_staging_replay_stress(cuda, monkeypatch):
     want = C.data.clone()
     monkeypatch.setenv("RECTRI_CU_SGEMM", "2")
     C0 = to_dev(c0).data.clone()
-    for rep in range(12):
-        C.data.copy_(C0)
-        gemm(-1.0, Trans.NoTrans, A.cview(), Trans.NoTrans, B.cview(), 1.0, C.view())
-        assert torch.equal(C.data, want), rep
+    for wide in ("0", "1"):  # 128x128 and 128x256 tiles
+        monkeypatch.setenv("RECTRI_CU_SGEMM_WIDE", wide)
+        for rep in range(12):
+            C.data.copy_(C0)
+            gemm(-1.0, Trans.NoTrans, A.cview(), Trans.NoTrans, B.cview(), 1.0, C.view())
+            assert torch.equal(C.data, want), (wide, rep)
 
