@@ -596,13 +596,16 @@ void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t 
   const int forced = e ? atoi(e) : 0;
   const int bk = forced == 16 || forced == 32 ? forced : (ta ? 16 : 32);
   // 128 x 256 tiles (8 x 16 per thread, one CTA per SM) for updates with at
-  // least four waves of them: +3-8 % on the long updates (fewer shared
+  // least a wave of them: +3-8 % on the long updates (fewer shared
   // wavefronts per FMA), but a quarter of the 128 x 128 CTAs per SM slot
   // would starve the short ones (fp32 TRSM n = 4096 1925 -> 2105 us if
-  // forced).  RECTRI_CU_SGEMM_WIDE = 0 / 1 forces it off / on.
+  // forced everywhere).  Threshold sweep 592 / 444 / 296 / 148 tiles: 148
+  // best (n = 8192 -1 %, 16384 -0.5 %, smaller n unchanged).
+  // RECTRI_CU_SGEMM_WIDE = 0 / 1 forces it off / on.
   const char* w = getenv("RECTRI_CU_SGEMM_WIDE");
   const i64 wide_tiles = ceil_div(p.M, 128) * ceil_div(p.N, 256);
-  const bool wide = w ? atoi(w) == 1 : wide_tiles >= 4 * 148;
+  const char* wm = getenv("RECTRI_CU_SGEMM_WIDE_MIN");  // tuning: tile-count threshold
+  const bool wide = w ? atoi(w) == 1 : wide_tiles >= (wm ? atoll(wm) : 148);
   if (sgemm_version() == 2 && wide && bk == 32) dispatch2<128, 256, 3, 32>(p, ta, tb, s);
   else if (sgemm_version() == 2 && wide) dispatch2<128, 256, 3>(p, ta, tb, s);
   else if (sgemm_version() == 2 && bk == 32) dispatch2<128, 128, 3, 32>(p, ta, tb, s);
