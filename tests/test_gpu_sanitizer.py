@@ -19,7 +19,12 @@ def _san(tool, args, env_extra=None):
     env.update(env_extra or {})
     cmd = [SAN, "--tool", tool, "--kernel-name", "kns=rectri_cu", "--print-limit", "5",
            sys.executable, str(ROOT / "tools" / "prof_run.py"), *args]
-    return subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    # GPU pools may close the tool (it exits 86 with a notice instead of
+    # running): nothing was checked, so the test is skipped, not passed.
+    if r.returncode == 86 and "closed" in (r.stdout + r.stderr):
+        pytest.skip("compute-sanitizer is closed on this GPU pool: " + (r.stdout + r.stderr).strip()[:160])
+    return r
 
 
 @pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
