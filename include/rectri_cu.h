@@ -194,6 +194,19 @@ int rectri_cu_make_dominant(int32_t dtype, rectri_cu_view A, int32_t uplo,
  * kind 0 = fp64 DMMA.8x8x4, 1 = fp32 FFMA.  Negative on failure. */
 double rectri_cu_probe_peak(int32_t kind);
 
+/* Ring checking of the default fp64 leaf (a diagnostic, not a reference
+ * entry point; the role of the reference's workgroup race detector,
+ * src/workgroup.cpp:138-177).  With RECTRI_CU_LEAF_CHECK=1 in the
+ * environment when a leaf is launched (or a graph captured), every A
+ * fragment a consumer warp reads from the leaf's mbarrier-guarded ring is
+ * compared with its packed block in global memory -- a refill overtaking a
+ * slot's readers shows up as a mismatch; =2 also plants a slot mix-up (the
+ * negative test).  Synchronises the device and returns the mismatch count
+ * (-1 if the counter cannot be allocated); reset != 0 zeroes it.  The first
+ * call allocates the counter: make it before the checked launches (a graph
+ * capture cannot allocate). */
+int64_t rectri_cu_debug_ring_check(int32_t reset);
+
 /* Per-kernel-class CUDA-event profiling.  While enabled, every call launches
  * directly (no graph) and brackets each launch with events on its stream.
  * rectri_cu_profile_read fills, for kinds 0 = GEMM, 1 = leaf, 2 = scale,

@@ -83,6 +83,7 @@ SIGNATURES = {
     "rectri_cu_fill_uniform": (ctypes.c_int, [c_i32, View, c_i64, c_i64, ctypes.c_uint64, _P(BackendC)]),
     "rectri_cu_make_dominant": (ctypes.c_int, [c_i32, View, c_i32, _P(BackendC)]),
     "rectri_cu_probe_peak": (ctypes.c_double, [c_i32]),
+    "rectri_cu_debug_ring_check": (c_i64, [c_i32]),
     "rectri_cu_profile_enable": (None, [c_i32]),
     "rectri_cu_profile_read": (ctypes.c_int, [_P(ctypes.c_double), _P(c_i64), _P(ctypes.c_double)]),
     "rectri_cu_bench_inputs_f64": (None, [ctypes.c_void_p, ctypes.c_void_p, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32,

@@ -593,6 +593,14 @@ def make_dominant(A: MatrixView, uplo: Uplo = Uplo.Lower, backend: Optional[Back
     raise_for_status(st, _lib.last_error() if st else "")
 
 
+def debug_ring_check(reset: bool = True) -> int:
+    """Mismatches the default fp64 leaf's ring checker counted
+    (RECTRI_CU_LEAF_CHECK=1 at launch / capture; =2 plants a slot mix-up);
+    synchronises the device.  The first call allocates the counter: call it
+    once before the checked launches."""
+    return int(_lib.load().rectri_cu_debug_ring_check(1 if reset else 0))
+
+
 def probe_peak(kind: str = "f64") -> float:
     """Measured issue-rate peak in TFLOP/s: 'f64' = DMMA.8x8x4, 'f32' = FFMA."""
     return float(_lib.load().rectri_cu_probe_peak(0 if kind == "f64" else 1))

@@ -1970,6 +1970,8 @@ int rectri_cu_make_dominant(int32_t dtype, rectri_cu_view A, int32_t uplo,
 
 double rectri_cu_probe_peak(int32_t kind) { return probe_peak_tflops(kind); }
 
+int64_t rectri_cu_debug_ring_check(int32_t reset) { return leaf_ring_check_read(reset != 0); }
+
 void rectri_cu_profile_enable(int32_t on) {
   std::lock_guard<std::mutex> lock(g_mu);
   g_prof.on = on != 0;

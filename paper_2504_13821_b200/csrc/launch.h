@@ -53,6 +53,12 @@ struct LeafParams {
   double* packed = nullptr;    // v3: this leaf's triangle already packed here (pack3_all_kernel)
   int pack_asc = 0;            // packed TRMM blocks in ascending row order (the v5 leaf's; TRSM always is)
   int direct = 0;              // a direct trmm_base / trsm_base call (not inside a recursion)
+  // Ring checking (RECTRI_CU_LEAF_CHECK, leaf64_v3.cu): every fragment a
+  // consumer warp read from a ring slot is compared with the packed block in
+  // global memory; mismatches are counted here.  ring_plant: the consumers
+  // read the wrong slot (the checker's negative test).
+  unsigned long long* ring_check = nullptr;
+  int ring_plant = 0;
 };
 
 constexpr int kLeafMax = 256;
@@ -119,6 +125,13 @@ double probe_peak_tflops(int kind);
 
 // Number of kernel launches issued (incremented by each launcher).
 i64& launch_counter();
+// RECTRI_CU_LEAF_CHECK = 1 (check) / 2 (check + planted slot mix-up): the
+// device mismatch counter the v3 leaves report to, else nullptr; plant is set
+// for mode 2.  leaf_ring_check_read synchronises the device and returns the
+// count (allocating the counter on the first call, which must precede the
+// checked launches), optionally resetting it.
+unsigned long long* leaf_ring_check_counter(int* plant);
+long long leaf_ring_check_read(bool reset);
 
 // Scratch a captured graph owns, by the stream its kernels are captured on:
 // the unpacked-leaf scratch (leaf64.cu) and the 3xTF32 operand splits

@@ -154,7 +154,8 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 // producer warp; each thread keeps 4 rows x 2 right-hand sides (one A read
 // feeds both columns) and the same k order for every NC, so the widths
 // agree bit for bit.
-template <int NC>
+// CK: the ring checker's instantiation (RECTRI_CU_LEAF_CHECK, as in leaf64_v3.cu).
+template <int NC, bool CK = false>
 __global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams<float> p,
                                                                 const float* __restrict__ P) {
   pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
@@ -251,7 +252,8 @@ __global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams
   auto block_mma = [&](const float* src0, const float* src1) {
     const int slot = s % kRing;
     mbar_wait(full0 + 8 * slot, (s / kRing) & 1);
-    const float* blk = ring + slot * kBlk;
+    const float* blk = ring + (CK && p.ring_plant ? (s + 1) % kRing : slot) * kBlk;
+    unsigned bad = 0;
 #pragma unroll
     for (int kb = 0; kb < kRB; kb += 4) {
       const float4 x0 = *reinterpret_cast<const float4*>(src0 + kb);
@@ -260,6 +262,11 @@ __global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const float4 a = *reinterpret_cast<const float4*>(blk + (kb + kk) * kRB + rw);  // broadcast
+        if (CK) {  // RECTRI_CU_LEAF_CHECK: block s's packed values, bit for bit
+          const float4 g = *reinterpret_cast<const float4*>(P + static_cast<size_t>(s) * kBlk + (kb + kk) * kRB + rw);
+          bad += (__float_as_uint(a.x) != __float_as_uint(g.x)) + (__float_as_uint(a.y) != __float_as_uint(g.y)) +
+                 (__float_as_uint(a.z) != __float_as_uint(g.z)) + (__float_as_uint(a.w) != __float_as_uint(g.w));
+        }
         unsigned long long a01, a23;
         asm("mov.b64 %0, {%1, %2};" : "=l"(a01) : "f"(a.x), "f"(a.y));
         asm("mov.b64 %0, {%1, %2};" : "=l"(a23) : "f"(a.z), "f"(a.w));
@@ -276,6 +283,7 @@ __global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams
     // address depends on the accumulators every loaded A value fed
     // (slot_dep, common.cuh; FFMA2 latency only, no proxy-fence MEMBAR)
     const uint32_t dep = slot_dep(dep0, acc[0][0], acc[0][1]);
+    if (CK && bad) atomicAdd(p.ring_check, static_cast<unsigned long long>(bad));
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * slot + dep);
     ++s;
@@ -371,7 +379,17 @@ void launch_leaf_f32_v3(const LeafParams<float>& p, float* scratch, cudaStream_t
     launch_kernel(kern, static_cast<unsigned>(ceil_div(p.nrhs, width)), 4 * width + 32, smem, s, p, scratch);
   };
   const int nc = leaf3_width(p.nrhs, p.trsm != 0);
-  if (nc == 32) go(leaf32_kernel<32>, 32, smem_bytes<32>());
+  LeafParams<float> q = p;
+  q.ring_check = leaf_ring_check_counter(&q.ring_plant);
+  if (q.ring_check) {
+    auto gc = [&](auto kern, int width, int smem) {
+      set_smem(kern, smem);
+      launch_kernel(kern, static_cast<unsigned>(ceil_div(p.nrhs, width)), 4 * width + 32, smem, s, q, scratch);
+    };
+    if (nc == 32) gc(leaf32_kernel<32, true>, 32, smem_bytes<32>());
+    else if (nc == 16) gc(leaf32_kernel<16, true>, 16, smem_bytes<16>());
+    else gc(leaf32_kernel<8, true>, 8, smem_bytes<8>());
+  } else if (nc == 32) go(leaf32_kernel<32>, 32, smem_bytes<32>());
   else if (nc == 16) go(leaf32_kernel<16>, 16, smem_bytes<16>());
   else go(leaf32_kernel<8>, 8, smem_bytes<8>());
   ++launch_counter();

@@ -217,7 +217,9 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 // WM = 2: a compute warp owns 2 row tiles x E column tiles (16 x 16 for
 // NC = 32, 4 compute warps): every A and B fragment feeds two DMMAs, a third
 // fewer shared-memory wavefronts per DMMA than WM = 1 (8 x 16 per warp).
-template <int NC, int WM = 1>
+// CK: the ring checker's instantiation (RECTRI_CU_LEAF_CHECK; the default
+// kernels carry no trace of it).
+template <int NC, int WM = 1, bool CK = false>
 __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParams<double> p,
                                                                 const double* __restrict__ P) {
   pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
@@ -340,13 +342,24 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
     if (!computes) return;
     const int slot = s % kRing;
     mbar_wait(full0 + 8 * slot, (s / kRing) & 1);
-    const uint32_t as = smem_u32(ring + slot * kBlk) + a_off;
+    // (ring_plant: the checker's negative test reads the next slot instead)
+    const uint32_t as = smem_u32(ring + (CK && p.ring_plant ? (s + 1) % kRing : slot) * kBlk) + a_off;
     double a[WM][8];
 #pragma unroll
     for (int i = 0; i < WM; ++i)
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[i][kk]) : "r"(as + (i * 8 + kk) * 32 * 8));
+    if (CK) {  // RECTRI_CU_LEAF_CHECK: the fragments must be block s's packed values
+      const double* src = P + static_cast<size_t>(s) * kBlk + a_off / 8;
+      unsigned bad = 0;
+#pragma unroll
+      for (int i = 0; i < WM; ++i)
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          bad += __double_as_longlong(a[i][kk]) != __double_as_longlong(src[(i * 8 + kk) * 32]) ? 1u : 0u;
+      if (bad) atomicAdd(p.ring_check, static_cast<unsigned long long>(bad));
+    }
     // all 8 k-steps' B fragments first: one shared-memory latency per block
     double bv[kRB / 4][E];
 #pragma unroll
@@ -484,6 +497,7 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
   const int nc = leaf3_width(p.nrhs, p.trsm != 0);
   const char* trv = getenv("RECTRI_CU_LEAF_TRACE");
   LeafParams<double> q = p;
+  q.ring_check = leaf_ring_check_counter(&q.ring_plant);
   long long* d_tr = nullptr;
   const unsigned grid = static_cast<unsigned>(ceil_div(p.nrhs, nc));
   if (trv && atoi(trv) && !prepacked) {
@@ -496,7 +510,11 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
     launch_kernel(kern, static_cast<unsigned>(ceil_div(p.nrhs, width)), kThreads + 32, smem, s, q, scratch);
   };
   const char* wm = getenv("RECTRI_CU_LEAF_WM");
-  if (nc == 32 && wm && atoi(wm) == 2) go(leaf3_kernel<32, 2>, 32, smem_bytes<32>());
+  if (q.ring_check) {
+    if (nc == 32) go(leaf3_kernel<32, 1, true>, 32, smem_bytes<32>());
+    else if (nc == 16) go(leaf3_kernel<16, 1, true>, 16, smem_bytes<16>());
+    else go(leaf3_kernel<8, 1, true>, 8, smem_bytes<8>());
+  } else if (nc == 32 && wm && atoi(wm) == 2) go(leaf3_kernel<32, 2>, 32, smem_bytes<32>());
   else if (nc == 32) go(leaf3_kernel<32>, 32, smem_bytes<32>());
   else if (nc == 16) go(leaf3_kernel<16>, 16, smem_bytes<16>());
   else go(leaf3_kernel<8>, 8, smem_bytes<8>());
@@ -514,6 +532,40 @@ void launch_leaf_f64_v3(const LeafParams<double>& p, double* scratch, cudaStream
     for (int bi = 0; bi < nblk; ++bi) fprintf(stderr, " %.0f", acc[2 + bi] / grid);
     fprintf(stderr, " | end %.0f\n", acc[41] / grid);
   }
+}
+
+namespace {
+// Allocated by the first leaf_ring_check_read (outside any graph capture:
+// the checked launches may be captured, an allocation there may not).
+unsigned long long* g_ring_counter = nullptr;
+}  // namespace
+
+unsigned long long* leaf_ring_check_counter(int* plant) {
+  const char* e = getenv("RECTRI_CU_LEAF_CHECK");
+  const int mode = e ? atoi(e) : 0;
+  *plant = mode == 2 ? 1 : 0;
+  if (mode != 1 && mode != 2) return nullptr;
+  if (!g_ring_counter) fprintf(stderr, "RECTRI_CU_LEAF_CHECK: call rectri_cu_debug_ring_check first; not checking\n");
+  return g_ring_counter;
+}
+
+long long leaf_ring_check_read(bool reset) {
+  cudaDeviceSynchronize();
+  if (!g_ring_counter) {
+    if (cudaMalloc(&g_ring_counter, sizeof(unsigned long long)) != cudaSuccess) {
+      g_ring_counter = nullptr;
+      return -1;
+    }
+    cudaMemset(g_ring_counter, 0, sizeof(unsigned long long));
+    cudaDeviceSynchronize();
+  }
+  unsigned long long h = 0;
+  cudaMemcpy(&h, g_ring_counter, sizeof(h), cudaMemcpyDeviceToHost);
+  if (reset) {
+    cudaMemset(g_ring_counter, 0, sizeof(h));
+    cudaDeviceSynchronize();
+  }
+  return static_cast<long long>(h);
 }
 
 }  // namespace rectri_cu

@@ -1,0 +1,68 @@
+"""Ring checking of the default leaves (leaf3_kernel, csrc/leaf64_v3.cu;
+leaf32_kernel, csrc/leaf32_v3.cu):
+the producer warp refills mbarrier-guarded shared-memory slots with
+cp.async.bulk while the compute warps read them, an ordering that
+compute-sanitizer racecheck does not model (and the tool may be closed on
+the GPU pool).  With RECTRI_CU_LEAF_CHECK=1 every A fragment a compute warp
+reads from a slot is compared, bit for bit, with its packed block in global
+memory: a refill that overtook the slot's readers would show up as a
+mismatch.  =2 plants a slot mix-up, which the checker must report -- the
+role of the reference's workgroup race detector and its planted race
+(src/workgroup.cpp:138-177, 333-349; tests/test_workgroup.cpp:144-176)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2504_13821_b200 import NO_GRAPH, Backend, Threshold, rec_trmm, rec_trsm
+from tests._util import check_against_oracle, to_dev, to_np, tspec
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(op, s, n, m, rng):
+    seed = int(rng.integers(1 << 30))
+    return (np.asfortranarray(oracle.make_operand(s, op == "trsm", n, seed)),
+            np.asfortranarray(oracle.make_rhs(s, n, m, seed + 1)))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("op", ["trsm", "trmm"])
+@pytest.mark.parametrize("width", ["8", "16", "32"])
+@pytest.mark.parametrize("side", [0, 1])
+def test_leaf_ring_check(cuda, monkeypatch, op, width, side, dtype):
+    import paper_2504_13821_b200 as rc
+    import torch
+
+    monkeypatch.setenv("RECTRI_CU_LEAF", "3")
+    monkeypatch.setenv("RECTRI_CU_LEAF_NC", width)
+    monkeypatch.setenv("RECTRI_CU_LEAF_CHECK", "1")
+    rc.clear_graph_cache()  # the checker instantiation is chosen at capture
+    rng = np.random.default_rng(700 + int(width) + 2 * side)
+    n, m = 1024, 2304
+    s = oracle.spec(side, 0, 0, 0, 1.0)
+    a, b = _inputs(op, s, n, m, rng)
+    a, b = np.asfortranarray(a.astype(dtype)), np.asfortranarray(b.astype(dtype))
+    A, B = to_dev(a), to_dev(b)
+    B0 = B.data.clone()
+    fn = rec_trmm if op == "trmm" else rec_trsm
+    rc.debug_ring_check(reset=True)
+    first = None
+    for rep in range(12):  # graph replays, then direct launches
+        B.data.copy_(B0)
+        be = Backend.cuda() if rep < 8 else Backend.cuda(flags=NO_GRAPH)
+        fn(tspec(s), A.cview(), B.view(), Threshold(256), be)
+        torch.cuda.synchronize()
+        if first is None:
+            first = B.data.clone()
+        else:
+            assert torch.equal(B.data, first), (op, width, rep)
+    assert rc.debug_ring_check(reset=True) == 0
+    check_against_oracle(op, s, a, b, to_np(B))
+
+    # planted slot mix-up: the checker must see it
+    monkeypatch.setenv("RECTRI_CU_LEAF_CHECK", "2")
+    rc.clear_graph_cache()
+    B.data.copy_(B0)
+    fn(tspec(s), A.cview(), B.view(), Threshold(256), Backend.cuda(flags=NO_GRAPH))
+    assert rc.debug_ring_check(reset=True) > 0
+    rc.clear_graph_cache()
