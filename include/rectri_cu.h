@@ -196,7 +196,7 @@ double rectri_cu_probe_peak(int32_t kind);
 
 /* Ring checking of the default fp64 leaf (a diagnostic, not a reference
  * entry point; the role of the reference's workgroup race detector,
- * src/workgroup.cpp:138-177).  With RECTRI_CU_LEAF_CHECK=1 in the
+ * src/workgroup.cpp:138-177).  With RECTRI_CU_RING_CHECK=1 in the
  * environment when a leaf is launched (or a graph captured), every A
  * fragment a consumer warp reads from the leaf's mbarrier-guarded ring is
  * compared with its packed block in global memory -- a refill overtaking a

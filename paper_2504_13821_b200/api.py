@@ -595,7 +595,7 @@ def make_dominant(A: MatrixView, uplo: Uplo = Uplo.Lower, backend: Optional[Back
 
 def debug_ring_check(reset: bool = True) -> int:
     """Mismatches the default fp64 leaf's ring checker counted
-    (RECTRI_CU_LEAF_CHECK=1 at launch / capture; =2 plants a slot mix-up);
+    (RECTRI_CU_RING_CHECK=1 at launch / capture; =2 plants a slot mix-up);
     synchronises the device.  The first call allocates the counter: call it
     once before the checked launches."""
     return int(_lib.load().rectri_cu_debug_ring_check(1 if reset else 0))

@@ -65,8 +65,10 @@ int choose_tma(const GemmParams<double>& p) {
   return !p.busy_gpu && tiles64 < small ? 3 : 1;
 }
 
-void launch_gemm_f64(const GemmParams<double>& p, bool ta, bool tb, cudaStream_t s) {
-  if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
+void launch_gemm_f64(const GemmParams<double>& p0, bool ta, bool tb, cudaStream_t s) {
+  if (p0.M <= 0 || p0.N <= 0 || p0.K <= 0) return;
+  GemmParams<double> p = p0;
+  p.ring_check = leaf_ring_check_counter(&p.ring_plant);  // RECTRI_CU_RING_CHECK (TMA kernels)
   const int cfg = choose_tma(p);
   if (cfg == 1 && launch_gemm_f64_split(p, ta, tb, s)) return;
   if (launch_gemm_f64_tma(p, ta, tb, s, cfg)) return;

@@ -107,7 +107,8 @@ bool split_launch(const GemmParams<double>& p, int n_main, cudaStream_t s) {
   if (!encode_operand(&a64, p.A, p.lda, p.M, p.K, 64, MC_A) || !encode_operand(&b64, p.B, p.ldb, p.N, p.K, 64, MC_B) ||
       !encode_operand(&a32, p.A, p.lda, p.M, p.K, 32, MC_A) || !encode_operand(&b32, p.B, p.ldb, p.N, p.K, 32, MC_B))
     return false;
-  auto kern = dgemm_tma::dgemm_tma_split_kernel<MC_A, MC_B>;
+  auto kern = p.ring_check ? dgemm_tma::dgemm_tma_split_kernel<MC_A, MC_B, true>
+                           : dgemm_tma::dgemm_tma_split_kernel<MC_A, MC_B>;
   const int smem = split_smem<MC_A, MC_B>();
   set_smem(kern, smem);
   const long long grid = ceil_div(p.M, 64) * (n_main / 64) + ceil_div(p.M, 32) * ceil_div(p.N - n_main, 32);

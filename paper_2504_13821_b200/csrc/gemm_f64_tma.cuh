@@ -103,7 +103,11 @@ __device__ __forceinline__ void lds128(double& x, double& y, uint32_t a) {
 // MC_A: A tile outer(m)-contiguous (op(A) = A); MC_B: B tile outer(n)-contiguous
 // (op(B) = B^T).
 // One BM x BN output tile at (m0, n0) (the body of every TMA DGEMM kernel).
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B>
+// CK: the ring checker's instantiation (RECTRI_CU_RING_CHECK): every fragment
+// a consumer warp reads from a stage is compared, bit for bit, with its
+// element of op(A) / op(B) in global memory (zero outside the matrix, as TMA
+// fills it); a refill overtaking a stage's readers shows up as a mismatch.
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B, bool CK = false>
 __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const CUtensorMap* mapB_,
                                                const GemmParams<double>& p, const int m0, const int n0,
                                                unsigned char* smem_raw) {
@@ -185,8 +189,9 @@ __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const C
   const uint32_t b_kc = static_cast<uint32_t>((wn0 + pg) * 128);
 
   double af[2][TM][2], bf[2][TN];
-  auto load_frags = [&](int buf, int s, int kk) {
-    const uint32_t as = stage_a(s), bs = stage_b(s);
+  auto load_frags = [&](int buf, int s, int kk, int ktile) {
+    const int sr = CK && p.ring_plant ? (s + 1) % STAGES : s;  // planted: the wrong stage
+    const uint32_t as = stage_a(sr), bs = stage_b(sr);
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
       if (MC_A) {
@@ -204,6 +209,30 @@ __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const C
 #pragma unroll
       for (int j = 0; j < TN; ++j) lds64(bf[buf][j], bs + b_kc + xo[kk] + (8 * j) * 128);
     }
+    if constexpr (CK) {
+      const i64 kg = static_cast<i64>(ktile) * kBK + 4 * kk + t;
+      auto opa = [&](i64 m) {
+        if (m >= p.M || kg >= p.K) return 0.0;
+        return MC_A ? p.A[m + kg * p.lda] : p.A[kg + m * p.lda];
+      };
+      auto opb = [&](i64 n) {
+        if (n >= p.N || kg >= p.K) return 0.0;
+        return MC_B ? p.B[n + kg * p.ldb] : p.B[kg + n * p.ldb];
+      };
+      auto ne = [](double x, double y) { return __double_as_longlong(x) != __double_as_longlong(y) ? 1u : 0u; };
+      unsigned bad = 0;
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const i64 m = m0 + wm0 + (MC_A ? 2 * g : pg) + 16 * i;
+        bad += ne(af[buf][i][0], opa(m)) + ne(af[buf][i][1], opa(MC_A ? m + 1 : m + 8));
+      }
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const i64 n = MC_B ? n0 + wn0 + 2 * g + 16 * (j / 2) + (j & 1) : n0 + wn0 + pg + 8 * j;
+        bad += ne(bf[buf][j], opb(n));
+      }
+      if (bad) atomicAdd(p.ring_check, static_cast<unsigned long long>(bad));
+    }
   };
 
   const uint32_t zero = static_cast<uint32_t>(p.K >> 40);  // 0 at run time, unknown to ptxas
@@ -217,7 +246,7 @@ __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const C
 
   if (KT > 0) {
     mbar_wait(full_bar(0), 0);
-    load_frags(0, 0, 0);
+    load_frags(0, 0, 0, 0);
   }
   for (int kt = 0; kt < KT; ++kt) {
     if (!PRODUCER && threadIdx.x == 0) {
@@ -232,11 +261,11 @@ __device__ __forceinline__ void dgemm_tma_tile(const CUtensorMap* mapA_, const C
     for (int kk = 0; kk < 4; ++kk) {
       const int cb = kk & 1, nb = cb ^ 1;
       if (kk < 3) {
-        load_frags(nb, s, kk + 1);
+        load_frags(nb, s, kk + 1, kt);
       } else if (kt + 1 < KT) {
         const int s1 = (kt + 1) % STAGES;
         mbar_wait(full_bar(s1), ((kt + 1) / STAGES) & 1);
-        load_frags(nb, s1, 0);
+        load_frags(nb, s1, 0, kt + 1);
       }
 #pragma unroll
       for (int i = 0; i < TM; ++i)
@@ -303,7 +332,7 @@ __device__ __forceinline__ void grouped_tile(int lin, int tiles_m, int tiles_n, 
   tn = in_grp / gsize;
 }
 
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B>
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool PRODUCER, bool MC_A, bool MC_B, bool CK = false>
 __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32, 1)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, const GemmParams<double> p) {
@@ -312,7 +341,8 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
   int tm, tn;
   grouped_tile(static_cast<int>(blockIdx.x), static_cast<int>(ceil_div(p.M, BM)), static_cast<int>(ceil_div(p.N, BN)),
                tm, tn);
-  dgemm_tma_tile<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B>(&mapA, &mapB, p, tm * BM, tn * BN, smem_raw);
+  dgemm_tma_tile<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B, CK>(&mapA, &mapB, p, tm * BM, tn * BN,
+                                                                             smem_raw);
 }
 
 // Wave-tail split: the columns [0, n_main) in 64x64 tiles -- a whole number
@@ -320,7 +350,7 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + (PRODUCER ? 1 : 0)) * 32,
 // CTAs per 64x64 tile, so the last wave is not a few long CTAs on a mostly
 // idle GPU.  Every element keeps the same k-tile order, so the result is bit
 // for bit that of the uniform kernels.
-template <bool MC_A, bool MC_B>
+template <bool MC_A, bool MC_B, bool CK = false>
 __global__ void __launch_bounds__(5 * 32, 1)
     dgemm_tma_split_kernel(const __grid_constant__ CUtensorMap a64, const __grid_constant__ CUtensorMap b64,
                            const __grid_constant__ CUtensorMap a32, const __grid_constant__ CUtensorMap b32,
@@ -333,12 +363,12 @@ __global__ void __launch_bounds__(5 * 32, 1)
   if (b < main_tiles) {
     int tm, tn;
     grouped_tile(b, tiles_m64, n_main / 64, tm, tn);
-    dgemm_tma_tile<64, 64, 2, 2, 4, true, MC_A, MC_B>(&a64, &b64, p, tm * 64, tn * 64, smem_raw);
+    dgemm_tma_tile<64, 64, 2, 2, 4, true, MC_A, MC_B, CK>(&a64, &b64, p, tm * 64, tn * 64, smem_raw);
   } else {
     const int tiles_m32 = static_cast<int>(ceil_div(p.M, 32));
     const int r = b - main_tiles;
-    dgemm_tma_tile<32, 32, 2, 2, 4, true, MC_A, MC_B>(&a32, &b32, p, (r % tiles_m32) * 32,
-                                                     n_main + (r / tiles_m32) * 32, smem_raw);
+    dgemm_tma_tile<32, 32, 2, 2, 4, true, MC_A, MC_B, CK>(&a32, &b32, p, (r % tiles_m32) * 32,
+                                                         n_main + (r / tiles_m32) * 32, smem_raw);
   }
 }
 

@@ -15,7 +15,8 @@ struct Config {
     CUtensorMap ma, mb;
     if (!encode_operand(&ma, p.A, p.lda, p.M, p.K, BM, MC_A)) return false;
     if (!encode_operand(&mb, p.B, p.ldb, p.N, p.K, BN, MC_B)) return false;
-    auto kern = dgemm_tma_kernel<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B>;
+    auto kern = p.ring_check ? dgemm_tma_kernel<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B, true>
+                             : dgemm_tma_kernel<BM, BN, WARPS_M, WARPS_N, STAGES, PRODUCER, MC_A, MC_B>;
     constexpr int slot_a = ((MC_A ? BM + 4 : BM) * kBK * 8 + 1023) / 1024 * 1024;
     constexpr int slot_b = ((MC_B ? BN + 4 : BN) * kBK * 8 + 1023) / 1024 * 1024;
     constexpr int smem = STAGES * (slot_a + slot_b) + 16 * STAGES + 1024;

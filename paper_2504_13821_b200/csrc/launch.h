@@ -25,6 +25,10 @@ struct GemmParams {
   // Scheduling hint (never changes a bit): 1 when other work runs beside this
   // update (TRMM's concurrent halves), so it keeps the large tiles.
   int busy_gpu = 0;
+  // Ring checking (RECTRI_CU_RING_CHECK, the TMA kernels' checker
+  // instantiation): mismatch counter and planted stage mix-up.
+  unsigned long long* ring_check = nullptr;
+  int ring_plant = 0;
 };
 
 // Leaf (base-kernel) problem in the reference's Left form on a virtual lower
@@ -53,7 +57,7 @@ struct LeafParams {
   double* packed = nullptr;    // v3: this leaf's triangle already packed here (pack3_all_kernel)
   int pack_asc = 0;            // packed TRMM blocks in ascending row order (the v5 leaf's; TRSM always is)
   int direct = 0;              // a direct trmm_base / trsm_base call (not inside a recursion)
-  // Ring checking (RECTRI_CU_LEAF_CHECK, leaf64_v3.cu): every fragment a
+  // Ring checking (RECTRI_CU_RING_CHECK, leaf64_v3.cu): every fragment a
   // consumer warp read from a ring slot is compared with the packed block in
   // global memory; mismatches are counted here.  ring_plant: the consumers
   // read the wrong slot (the checker's negative test).
@@ -125,7 +129,7 @@ double probe_peak_tflops(int kind);
 
 // Number of kernel launches issued (incremented by each launcher).
 i64& launch_counter();
-// RECTRI_CU_LEAF_CHECK = 1 (check) / 2 (check + planted slot mix-up): the
+// RECTRI_CU_RING_CHECK = 1 (check) / 2 (check + planted slot mix-up): the
 // device mismatch counter the v3 leaves report to, else nullptr; plant is set
 // for mode 2.  leaf_ring_check_read synchronises the device and returns the
 // count (allocating the counter on the first call, which must precede the

@@ -154,7 +154,7 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 // producer warp; each thread keeps 4 rows x 2 right-hand sides (one A read
 // feeds both columns) and the same k order for every NC, so the widths
 // agree bit for bit.
-// CK: the ring checker's instantiation (RECTRI_CU_LEAF_CHECK, as in leaf64_v3.cu).
+// CK: the ring checker's instantiation (RECTRI_CU_RING_CHECK, as in leaf64_v3.cu).
 template <int NC, bool CK = false>
 __global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams<float> p,
                                                                 const float* __restrict__ P) {
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(4 * NC + 32, 4) leaf32_kernel(const LeafParams
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const float4 a = *reinterpret_cast<const float4*>(blk + (kb + kk) * kRB + rw);  // broadcast
-        if (CK) {  // RECTRI_CU_LEAF_CHECK: block s's packed values, bit for bit
+        if (CK) {  // RECTRI_CU_RING_CHECK: block s's packed values, bit for bit
           const float4 g = *reinterpret_cast<const float4*>(P + static_cast<size_t>(s) * kBlk + (kb + kk) * kRB + rw);
           bad += (__float_as_uint(a.x) != __float_as_uint(g.x)) + (__float_as_uint(a.y) != __float_as_uint(g.y)) +
                  (__float_as_uint(a.z) != __float_as_uint(g.z)) + (__float_as_uint(a.w) != __float_as_uint(g.w));

@@ -217,7 +217,7 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 // WM = 2: a compute warp owns 2 row tiles x E column tiles (16 x 16 for
 // NC = 32, 4 compute warps): every A and B fragment feeds two DMMAs, a third
 // fewer shared-memory wavefronts per DMMA than WM = 1 (8 x 16 per warp).
-// CK: the ring checker's instantiation (RECTRI_CU_LEAF_CHECK; the default
+// CK: the ring checker's instantiation (RECTRI_CU_RING_CHECK; the default
 // kernels carry no trace of it).
 template <int NC, int WM = 1, bool CK = false>
 __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParams<double> p,
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) leaf3_kernel(const LeafParam
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[i][kk]) : "r"(as + (i * 8 + kk) * 32 * 8));
-    if (CK) {  // RECTRI_CU_LEAF_CHECK: the fragments must be block s's packed values
+    if (CK) {  // RECTRI_CU_RING_CHECK: the fragments must be block s's packed values
       const double* src = P + static_cast<size_t>(s) * kBlk + a_off / 8;
       unsigned bad = 0;
 #pragma unroll
@@ -541,11 +541,11 @@ unsigned long long* g_ring_counter = nullptr;
 }  // namespace
 
 unsigned long long* leaf_ring_check_counter(int* plant) {
-  const char* e = getenv("RECTRI_CU_LEAF_CHECK");
+  const char* e = getenv("RECTRI_CU_RING_CHECK");
   const int mode = e ? atoi(e) : 0;
   *plant = mode == 2 ? 1 : 0;
   if (mode != 1 && mode != 2) return nullptr;
-  if (!g_ring_counter) fprintf(stderr, "RECTRI_CU_LEAF_CHECK: call rectri_cu_debug_ring_check first; not checking\n");
+  if (!g_ring_counter) fprintf(stderr, "RECTRI_CU_RING_CHECK: call rectri_cu_debug_ring_check first; not checking\n");
   return g_ring_counter;
 }
 

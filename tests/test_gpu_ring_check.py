@@ -3,7 +3,7 @@ leaf32_kernel, csrc/leaf32_v3.cu):
 the producer warp refills mbarrier-guarded shared-memory slots with
 cp.async.bulk while the compute warps read them, an ordering that
 compute-sanitizer racecheck does not model (and the tool may be closed on
-the GPU pool).  With RECTRI_CU_LEAF_CHECK=1 every A fragment a compute warp
+the GPU pool).  With RECTRI_CU_RING_CHECK=1 every A fragment a compute warp
 reads from a slot is compared, bit for bit, with its packed block in global
 memory: a refill that overtook the slot's readers would show up as a
 mismatch.  =2 plants a slot mix-up, which the checker must report -- the
@@ -35,7 +35,7 @@ def test_leaf_ring_check(cuda, monkeypatch, op, width, side, dtype):
 
     monkeypatch.setenv("RECTRI_CU_LEAF", "3")
     monkeypatch.setenv("RECTRI_CU_LEAF_NC", width)
-    monkeypatch.setenv("RECTRI_CU_LEAF_CHECK", "1")
+    monkeypatch.setenv("RECTRI_CU_RING_CHECK", "1")
     rc.clear_graph_cache()  # the checker instantiation is chosen at capture
     rng = np.random.default_rng(700 + int(width) + 2 * side)
     n, m = 1024, 2304
@@ -60,9 +60,50 @@ def test_leaf_ring_check(cuda, monkeypatch, op, width, side, dtype):
     check_against_oracle(op, s, a, b, to_np(B))
 
     # planted slot mix-up: the checker must see it
-    monkeypatch.setenv("RECTRI_CU_LEAF_CHECK", "2")
+    monkeypatch.setenv("RECTRI_CU_RING_CHECK", "2")
     rc.clear_graph_cache()
     B.data.copy_(B0)
     fn(tspec(s), A.cview(), B.view(), Threshold(256), Backend.cuda(flags=NO_GRAPH))
     assert rc.debug_ring_check(reset=True) > 0
     rc.clear_graph_cache()
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_dgemm_ring_check(cuda, monkeypatch, ta, tb):
+    """The TMA DGEMM (dgemm_tma_kernel / dgemm_tma_split_kernel, the
+    recursion's off-diagonal updates): every A / B fragment a consumer warp
+    reads from a TMA-filled stage equals its element of op(A) / op(B) (zero
+    outside the matrix), on ragged shapes and the 64x64, 32x32 and wave-tail
+    split configurations; the result is bitwise the unchecked kernel's, and a
+    planted stage mix-up is reported."""
+    import paper_2504_13821_b200 as rc
+    import torch
+    from paper_2504_13821_b200 import Trans
+
+    rng = np.random.default_rng(40 + 2 * ta + tb)
+    rc.debug_ring_check(reset=True)
+
+    def run(a, b, c):
+        A, B, C = to_dev(np.asfortranarray(a)), to_dev(np.asfortranarray(b)), to_dev(np.asfortranarray(c))
+        rc.gemm(-1.0, Trans(ta), A.cview(), Trans(tb), B.cview(), 1.0, C.view(), Backend.cuda(flags=NO_GRAPH))
+        torch.cuda.synchronize()
+        return to_np(C)
+
+    for M, N, K, split in ((130, 70, 50, "1"), (1000, 3000, 700, "1"), (512, 8192, 256, "1"), (4096, 4096, 1024, "2"),
+                           (64, 64, 2048, "1")):
+        monkeypatch.setenv("RECTRI_CU_GEMM64_SPLIT", split)
+        a = rng.uniform(-1, 1, (K, M) if ta else (M, K))
+        b = rng.uniform(-1, 1, (N, K) if tb else (K, N))
+        c = rng.uniform(-1, 1, (M, N))
+        monkeypatch.setenv("RECTRI_CU_RING_CHECK", "0")
+        plain = run(a, b, c)
+        monkeypatch.setenv("RECTRI_CU_RING_CHECK", "1")
+        checked = run(a, b, c)
+        assert rc.debug_ring_check(reset=True) == 0, (M, N, K, split)
+        assert oracle.bitwise_equal(plain, checked), (M, N, K)
+        ref = c - (a.T if ta else a) @ (b.T if tb else b)
+        assert np.max(np.abs(checked - ref)) <= 64 * K * np.finfo(float).eps * (1 + np.max(np.abs(ref)))
+        if (M, N, K) == (1000, 3000, 700):  # planted stage mix-up
+            monkeypatch.setenv("RECTRI_CU_RING_CHECK", "2")
+            run(a, b, c)
+            assert rc.debug_ring_check(reset=True) > 0
