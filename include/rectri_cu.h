@@ -194,14 +194,15 @@ int rectri_cu_make_dominant(int32_t dtype, rectri_cu_view A, int32_t uplo,
  * kind 0 = fp64 DMMA.8x8x4, 1 = fp32 FFMA.  Negative on failure. */
 double rectri_cu_probe_peak(int32_t kind);
 
-/* Ring checking of the default fp64 leaf (a diagnostic, not a reference
- * entry point; the role of the reference's workgroup race detector,
- * src/workgroup.cpp:138-177).  With RECTRI_CU_RING_CHECK=1 in the
- * environment when a leaf is launched (or a graph captured), every A
- * fragment a consumer warp reads from the leaf's mbarrier-guarded ring is
- * compared with its packed block in global memory -- a refill overtaking a
- * slot's readers shows up as a mismatch; =2 also plants a slot mix-up (the
- * negative test).  Synchronises the device and returns the mismatch count
+/* Ring checking of the mbarrier-guarded shared-memory rings (a diagnostic,
+ * not a reference entry point; the role of the reference's workgroup race
+ * detector, src/workgroup.cpp:138-177).  With RECTRI_CU_RING_CHECK=1 in the
+ * environment when a kernel is launched (or a graph captured), the fp64 /
+ * fp32 v3 leaves, the TMA DGEMM and the fp32 FFMA2 GEMM compare every
+ * fragment a consumer warp reads from a stage with the element the stage
+ * must hold (packed block / op(A), op(B) in global memory) -- a refill
+ * overtaking a stage's readers shows up as a mismatch; =2 also plants a
+ * stage mix-up (the negative test).  Synchronises the device and returns the mismatch count
  * (-1 if the counter cannot be allocated); reset != 0 zeroes it.  The first
  * call allocates the counter: make it before the checked launches (a graph
  * capture cannot allocate). */

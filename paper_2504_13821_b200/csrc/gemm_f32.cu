@@ -326,7 +326,11 @@ __device__ __forceinline__ int outer_k(int t, int j) { return (j / 4) * (BO / (C
 // FFMA2 instead of 4 for 32 -- the shared-memory wavefronts, not the FMA
 // pipe, bound the 8 x 8 tile (ncu: 76 % of shared bandwidth at 85 % FMA).
 // Same k-ascending chain per element either way: bitwise equal.
-template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB, int BK = kBK>
+// CK: the ring checker's instantiation (RECTRI_CU_RING_CHECK): each k-step's
+// fragments are compared, bit for bit, with their op(A) / op(B) elements in
+// global memory (zero outside the matrix, as the loaders fill them) before
+// they are used; ring_plant reads the wrong stage (the negative test).
+template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB, int BK = kBK, bool CK = false>
 __global__ void __launch_bounds__(256, BN == 128 ? 2 : 1) sgemm_ffma2_kernel(const GemmParams<float> p) {
   pdl_wait();  // PDL: no-op unless launched programmatically (launch_kernel)
   constexpr int TX = 16, NT = 256;
@@ -394,15 +398,17 @@ __global__ void __launch_bounds__(256, BN == 128 ? 2 : 1) sgemm_ffma2_kernel(con
   for (int s = 0; s < STAGES; ++s)
     if (s < KT) fill(s, s);
   float fa[2][8], fb[2][CN];
+  // stage a consumer reads (CK && ring_plant: the next one, the planted mix-up)
+  auto rs_of = [&](int stage) { return CK && p.ring_plant ? (stage + 1) % STAGES : stage; };
   bar_wait(full0, 0);
-  read_k<BM>(sA, ty, 0, fa[0]);
-  read_k<BN, CN>(sB, tx, 0, fb[0]);
+  read_k<BM>(sA + rs_of(0) * A_EL, ty, 0, fa[0]);
+  read_k<BN, CN>(sB + rs_of(0) * B_EL, tx, 0, fb[0]);
   int st = 0;
   const uint32_t dep0 = static_cast<uint32_t>(p.K >> 40);  // 0 at run time, unknown to ptxas
   for (i64 kt = 0; kt < KT; ++kt) {
     const int cur = st;
-    const float* a_s = sA + st * A_EL;
-    const float* b_s = sB + st * B_EL;
+    const float* a_s = sA + rs_of(st) * A_EL;
+    const float* b_s = sB + rs_of(st) * B_EL;
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
       const int cb = k & 1;
@@ -420,9 +426,26 @@ __global__ void __launch_bounds__(256, BN == 128 ? 2 : 1) sgemm_ffma2_kernel(con
         st = st + 1 == STAGES ? 0 : st + 1;
         if (kt + 1 < KT) {
           bar_wait(full0 + 8 * st, static_cast<uint32_t>(((kt + 1) / STAGES) & 1));
-          read_k<BM>(sA + st * A_EL, ty, 0, fa[cb ^ 1]);
-          read_k<BN, CN>(sB + st * B_EL, tx, 0, fb[cb ^ 1]);
+          read_k<BM>(sA + rs_of(st) * A_EL, ty, 0, fa[cb ^ 1]);
+          read_k<BN, CN>(sB + rs_of(st) * B_EL, tx, 0, fb[cb ^ 1]);
         }
+      }
+      if constexpr (CK) {  // RECTRI_CU_RING_CHECK: fragments of (kt, k) vs op(A) / op(B)
+        const i64 kg = kt * BK + k;
+        unsigned bad = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const i64 m = m0 + outer_k<BM>(ty, j);
+          const float e = m < p.M && kg < p.K ? (TA ? p.A[kg + m * p.lda] : p.A[m + kg * p.lda]) : 0.f;
+          bad += __float_as_uint(fa[cb][j]) != __float_as_uint(e) ? 1u : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < CN; ++j) {
+          const i64 n = n0 + outer_k<BN, CN>(tx, j);
+          const float e = n < p.N && kg < p.K ? (TB ? p.B[n + kg * p.ldb] : p.B[kg + n * p.ldb]) : 0.f;
+          bad += __float_as_uint(fb[cb][j]) != __float_as_uint(e) ? 1u : 0u;
+        }
+        if (bad) atomicAdd(p.ring_check, static_cast<unsigned long long>(bad));
       }
 #pragma unroll
       for (int ip = 0; ip < 4; ++ip) {
@@ -513,7 +536,10 @@ __global__ void __launch_bounds__(256, BN == 128 ? 2 : 1) sgemm_ffma2_kernel(con
 
 template <int BM, int BN, int STAGES, bool TA, bool TB, int VA, int VB, int BK = kBK>
 void launch_cfg2(const GemmParams<float>& p, cudaStream_t s) {
-  auto kern = sgemm_ffma2_kernel<BM, BN, STAGES, TA, TB, VA, VB, BK>;
+  // the checker instantiation only for the vectorised copies (RECTRI_CU_RING_CHECK)
+  constexpr bool kCk = VA == 4 && VB == 4;
+  auto kern = kCk && p.ring_check ? sgemm_ffma2_kernel<BM, BN, STAGES, TA, TB, VA, VB, BK, kCk>
+                                  : sgemm_ffma2_kernel<BM, BN, STAGES, TA, TB, VA, VB, BK>;
   constexpr int smem = STAGES * BK * (BM + BN + 2 * kPadMC) * static_cast<int>(sizeof(float));
   set_smem(kern, smem);
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, BM)), static_cast<unsigned>(ceil_div(p.N, BN)));
@@ -586,8 +612,10 @@ int sgemm_version() {
 
 }  // namespace
 
-void launch_gemm_f32(const GemmParams<float>& p, bool ta, bool tb, cudaStream_t s) {
-  if (p.M <= 0 || p.N <= 0 || p.K <= 0) return;
+void launch_gemm_f32(const GemmParams<float>& p0, bool ta, bool tb, cudaStream_t s) {
+  if (p0.M <= 0 || p0.N <= 0 || p0.K <= 0) return;
+  GemmParams<float> p = p0;
+  p.ring_check = leaf_ring_check_counter(&p.ring_plant);  // RECTRI_CU_RING_CHECK (v2 kernels)
   if (tf32x3_enabled() && launch_gemm_f32_tf32x3(p, ta, tb, s)) return;
   // k-tile depth: 32 for op-N A (fewer barriers; NN +2 %, NT +5 % at
   // 8192x16384x8192), 16 for op-T A (two transposed operands at 32 spill).

@@ -107,3 +107,44 @@ def test_dgemm_ring_check(cuda, monkeypatch, ta, tb):
             monkeypatch.setenv("RECTRI_CU_RING_CHECK", "2")
             run(a, b, c)
             assert rc.debug_ring_check(reset=True) > 0
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_sgemm_ring_check(cuda, monkeypatch, ta, tb):
+    """The fp32 FFMA2 GEMM (sgemm_ffma2_kernel: cp.async stages with
+    per-stage mbarriers and a deferred refill): each k-step's A / B fragments
+    equal their op(A) / op(B) elements (zero outside the matrix) on the
+    128x128 and 128x256 tiles and both k-tile depths; bitwise the unchecked
+    kernel's result; a planted stage mix-up is reported."""
+    import paper_2504_13821_b200 as rc
+    import torch
+    from paper_2504_13821_b200 import Trans
+
+    rng = np.random.default_rng(60 + 2 * ta + tb)
+    rc.debug_ring_check(reset=True)
+
+    def run(a, b, c):
+        A, B, C = to_dev(np.asfortranarray(a)), to_dev(np.asfortranarray(b)), to_dev(np.asfortranarray(c))
+        rc.gemm(-1.0, Trans(ta), A.cview(), Trans(tb), B.cview(), 1.0, C.view(), Backend.cuda(flags=NO_GRAPH))
+        torch.cuda.synchronize()
+        return to_np(C)
+
+    for M, N, K, bk in ((128, 72, 52, "16"), (1000, 3000, 700, "32"), (512, 8192, 256, "16"), (4096, 4096, 1024, "32"),
+                        (4096, 4096, 1000, "16")):
+        monkeypatch.setenv("RECTRI_CU_SGEMM_BK", bk)
+        a = rng.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
+        b = rng.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
+        c = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+        monkeypatch.setenv("RECTRI_CU_RING_CHECK", "0")
+        plain = run(a, b, c)
+        monkeypatch.setenv("RECTRI_CU_RING_CHECK", "1")
+        checked = run(a, b, c)
+        assert rc.debug_ring_check(reset=True) == 0, (M, N, K, bk)
+        assert oracle.bitwise_equal(plain, checked), (M, N, K)
+        ref = c.astype(float) - (a.T if ta else a).astype(float) @ (b.T if tb else b).astype(float)
+        assert np.max(np.abs(checked - ref)) <= 8 * K * np.finfo(np.float32).eps * (1 + np.max(np.abs(ref)))
+        if (M, N, K) == (1000, 3000, 700):  # planted stage mix-up
+            monkeypatch.setenv("RECTRI_CU_RING_CHECK", "2")
+            run(a, b, c)
+            assert rc.debug_ring_check(reset=True) > 0
+
