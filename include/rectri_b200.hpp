@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdint>
 #include <functional>
+#include <new>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -142,6 +143,29 @@ inline std::string variant_string(const TriangularSpec& s) {
 // ---- storage and windows ----------------------------------------------------
 template <typename T> class MatrixView;
 
+// Storage allocator of MatrixBuffer: rectri_cu_host_alloc -- page-locked
+// memory when a CUDA device is present (RECTRI_CU_PINNED_BUFFERS=0: plain
+// malloc), so rec_trsm / rec_trmm on MatrixBuffers copy them at full PCIe
+// rate with no bounce through a staging buffer.  The buffer's interface is
+// the reference's (matrix.hpp:18-70); only where its bytes live changes.
+template <typename T>
+struct HostAllocator {
+  using value_type = T;
+  HostAllocator() noexcept = default;
+  template <typename U>
+  HostAllocator(const HostAllocator<U>&) noexcept {}
+  T* allocate(std::size_t n) {
+    void* p = rectri_cu_host_alloc(n * sizeof(T), nullptr);
+    if (!p) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, std::size_t) noexcept { rectri_cu_host_free(p); }
+  template <typename U>
+  bool operator==(const HostAllocator<U>&) const noexcept { return true; }
+  template <typename U>
+  bool operator!=(const HostAllocator<U>&) const noexcept { return false; }
+};
+
 template <typename T>
 class MatrixBuffer {
   static_assert(std::is_floating_point_v<T>);
@@ -177,7 +201,7 @@ class MatrixBuffer {
 
  private:
   index_t rows_ = 0, cols_ = 0;
-  std::vector<T> store_;
+  std::vector<T, HostAllocator<T>> store_;
 };
 
 // Window of an origin buffer (host or device), column-major, ld = origin rows.

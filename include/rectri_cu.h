@@ -36,6 +36,7 @@
 #ifndef RECTRI_CU_H_
 #define RECTRI_CU_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -207,6 +208,16 @@ double rectri_cu_probe_peak(int32_t kind);
  * call allocates the counter: make it before the checked launches (a graph
  * capture cannot allocate). */
 int64_t rectri_cu_debug_ring_check(int32_t reset);
+
+/* Host storage of the C++ drop-in's MatrixBuffer (include/rectri_b200.hpp;
+ * the reference's std::vector storage, include/rectri/matrix.hpp:18-70):
+ * page-locked when a CUDA device is present and RECTRI_CU_PINNED_BUFFERS is
+ * not 0 (*pinned = 1), so host-resident operands in MatrixBuffers move at
+ * full PCIe rate without a bounce copy; plain malloc otherwise.  NULL on
+ * failure.  rectri_cu_host_free releases a pointer from rectri_cu_host_alloc
+ * (and ignores anything else). */
+void* rectri_cu_host_alloc(size_t bytes, int32_t* pinned);
+void rectri_cu_host_free(void* p);
 
 /* Per-kernel-class CUDA-event profiling.  While enabled, every call launches
  * directly (no graph) and brackets each launch with events on its stream.

@@ -1972,6 +1972,54 @@ double rectri_cu_probe_peak(int32_t kind) { return probe_peak_tflops(kind); }
 
 int64_t rectri_cu_debug_ring_check(int32_t reset) { return leaf_ring_check_read(reset != 0); }
 
+// Host storage for the C++ drop-in's MatrixBuffer: page-locked (portable)
+// when a CUDA device is present and RECTRI_CU_PINNED_BUFFERS is not 0, so the
+// host-operand path moves it at full PCIe rate with no bounce copy; plain
+// malloc otherwise (or when pinning fails).  Allocations are remembered so
+// rectri_cu_host_free releases each the way it was made.
+namespace {
+std::mutex g_host_mu;
+std::map<void*, bool> g_host_allocs;  // pointer -> page-locked
+}  // namespace
+
+void* rectri_cu_host_alloc(size_t bytes, int32_t* pinned) {
+  if (pinned) *pinned = 0;
+  if (bytes == 0) bytes = 1;
+  void* p = nullptr;
+  bool pin = false;
+  const char* e = getenv("RECTRI_CU_PINNED_BUFFERS");
+  int ndev = 0;
+  if (!(e && atoi(e) == 0) && cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
+    pin = cudaHostAlloc(&p, bytes, cudaHostAllocPortable) == cudaSuccess;
+    if (!pin) {
+      p = nullptr;
+      cudaGetLastError();  // clear the failed allocation's error
+    }
+  }
+  if (!p) p = std::malloc(bytes);
+  if (!p) return nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    g_host_allocs[p] = pin;
+  }
+  if (pinned) *pinned = pin ? 1 : 0;
+  return p;
+}
+
+void rectri_cu_host_free(void* p) {
+  if (!p) return;
+  bool pin = false;
+  {
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    auto it = g_host_allocs.find(p);
+    if (it == g_host_allocs.end()) return;
+    pin = it->second;
+    g_host_allocs.erase(it);
+  }
+  if (pin) cudaFreeHost(p);
+  else std::free(p);
+}
+
 void rectri_cu_profile_enable(int32_t on) {
   std::lock_guard<std::mutex> lock(g_mu);
   g_prof.on = on != 0;

@@ -1,11 +1,16 @@
-// End-to-end timing through the C++ drop-in with the reference caller's own
-// memory: std::vector-backed rectri::MatrixBuffer (include/rectri/matrix.hpp,
-// as src/bench.cpp:184-192 allocates it), i.e. PAGEABLE host buffers.  Each
-// timed call is rectri::rec_trsm<double> exactly as reference code writes it;
-// the library stages A and B through its pinned bounce buffers, computes on
-// the GPU and writes X back into the vectors before returning.
+// End-to-end timing through the C++ drop-in with reference-caller memory.
+// Each timed call is rectri::rec_trsm<double> exactly as reference code
+// writes it (src/bench.cpp:184-192).  Two storages:
+//   buffer    rectri::MatrixBuffer, as the reference's callers allocate it --
+//             the drop-in's MatrixBuffer keeps its bytes page-locked
+//             (rectri_cu_host_alloc), so the library streams them directly;
+//   pageable  plain std::vector<double> wrapped in MatrixViews (the public
+//             MatrixView constructor, matrix.hpp:82-90): PAGEABLE memory the
+//             library stages through its pinned bounce buffers.
+// Either way the library computes on the GPU and writes X back into host
+// memory before returning.
 //
-//   dropin_bench N M STEPS WARMUP   -> one JSON line on stdout
+//   dropin_bench N M STEPS WARMUP [buffer|pageable]   -> one JSON line on stdout
 //
 // B is restored from a pristine copy between calls, outside the clock
 // (bench.cpp:184-218 methodology: steady_clock around the call).  A sampled
@@ -18,6 +23,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <limits>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -53,7 +59,16 @@ int main(int argc, char** argv) {
   const int steps = argc > 3 ? std::atoi(argv[3]) : 5;
   const int warmup = argc > 4 ? std::atoi(argv[4]) : 2;
 
-  MatrixBuffer<double> A(n, n), B(n, m), B0(n, m);
+  const bool pageable = argc > 5 && std::string(argv[5]) == "pageable";
+  // storage: MatrixBuffers, or plain vectors behind views of the same shape
+  MatrixBuffer<double> Ab(pageable ? 0 : n, pageable ? 0 : n), Bb(pageable ? 0 : n, pageable ? 0 : m),
+      B0b(pageable ? 0 : n, pageable ? 0 : m);
+  std::vector<double> Av(pageable ? static_cast<size_t>(n * n) : 0), Bv(pageable ? static_cast<size_t>(n * m) : 0),
+      B0v(pageable ? static_cast<size_t>(n * m) : 0);
+  auto mk = [&](MatrixBuffer<double>& b, std::vector<double>& v, index_t r, index_t c) {
+    return pageable ? MatrixView<double>(v.data(), r, c, 0, 0, r, c) : b.view();
+  };
+  const MatrixView<double> A = mk(Ab, Av, n, n), B = mk(Bb, Bv, n, m), B0 = mk(B0b, B0v, n, m);
   parallel_cols(n, [&](index_t c) {
     for (index_t r = 0; r < n; ++r) A(r, c) = uniform(1000003ull * c + r);
   });
@@ -73,7 +88,7 @@ int main(int argc, char** argv) {
   for (int i = 0; i < warmup + steps; ++i) {
     parallel_cols(m, [&](index_t c) { std::copy(&B0(0, c), &B0(0, c) + n, &B(0, c)); });
     const auto t0 = std::chrono::steady_clock::now();
-    rec_trsm<double>(spec, A.view(), B.view(), Threshold{256});
+    rec_trsm<double>(spec, MatrixView<const double>(A), B, Threshold{256});
     const auto t1 = std::chrono::steady_clock::now();
     if (i >= warmup) ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
   }
@@ -99,9 +114,10 @@ int main(int argc, char** argv) {
   for (double v : ms) sum += v;
   std::vector<double> sorted = ms;
   std::sort(sorted.begin(), sorted.end());
-  std::printf("{\"n\": %lld, \"m\": %lld, \"steps\": %d, \"ms_per_step\": %.3f, \"median_step_ms\": %.3f, "
-              "\"eta\": %.3e, \"finite\": %s, \"step_ms\": [",
-              static_cast<long long>(n), static_cast<long long>(m), steps, sum / ms.size(),
+  std::printf("{\"storage\": \"%s\", \"n\": %lld, \"m\": %lld, \"steps\": %d, \"ms_per_step\": %.3f, "
+              "\"median_step_ms\": %.3f, \"eta\": %.3e, \"finite\": %s, \"step_ms\": [",
+              pageable ? "pageable" : "buffer", static_cast<long long>(n), static_cast<long long>(m), steps,
+              sum / ms.size(),
               sorted[sorted.size() / 2], eta, finite ? "true" : "false");
   for (size_t i = 0; i < ms.size(); ++i) std::printf("%s%.2f", i ? ", " : "", ms[i]);
   std::printf("]}\n");
