@@ -585,14 +585,26 @@ bool conc_enabled() {
 
 // Streams the right-hand sides are split over (RECTRI_CU_STREAMS, default 2;
 // panels narrower than 2048 right-hand sides are not split).
-int panel_streams(i64 rhs) {
+// Right-hand-side streams of a call: `pref` (RECTRI_CU_STREAMS overrides),
+// fewer when the panels would drop below RECTRI_CU_PANEL_MIN columns.
+int panel_streams(i64 rhs, int pref = 2) {
   const char* e = getenv("RECTRI_CU_STREAMS");
-  int p = e ? atoi(e) : 2;
+  int p = e ? atoi(e) : pref;
   if (p > DeviceRes::kAux + 1) p = DeviceRes::kAux + 1;
   const char* w = getenv("RECTRI_CU_PANEL_MIN");
   const i64 min_w = w && atoll(w) > 0 ? atoll(w) : 2048;
   while (p > 1 && rhs / p < min_w) --p;
   return p < 1 ? 1 : p;
+}
+
+// Device-resident graphs: three right-hand-side streams for fp64 calls with
+// >= 8192 right-hand sides, two otherwise (fp64 small_probe, one B200:
+// TRMM n = m = 8192 16036 -> 15972 us, 16384 124147 -> 123871 us; TRSM 8192
+// 16110 -> 16075, 16384 124340 -> 124193; at 4096 a third stream costs TRMM
+// 3 %; fp32 and the streamed host path keep two; profiles/r02_streams*.txt).
+template <typename T>
+int device_streams_pref(i64 rhs) {
+  return sizeof(T) == 8 && rhs >= 8192 ? 3 : 2;
 }
 
 void* staging(DeviceRes& r, int slot, size_t bytes) {
@@ -771,7 +783,7 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
   ConcCtx<T> conc;
   const bool left_ = spec.side == RECTRI_CU_LEFT;
   const i64 rhs_ = left_ ? B.cols : B.rows;
-  const int P_ = g_prof.on ? 1 : panel_streams(rhs_);
+  const int P_ = g_prof.on ? 1 : panel_streams(rhs_, device_streams_pref<T>(rhs_));
   // Only where the GPU is not already full: n <= 4096 (fp64) / 8192 (fp32).
   i64 conc_max_n = sizeof(T) == 8 ? 4096 : 8192;
   if (const char* e = getenv("RECTRI_CU_TRMM_CONC_MAXN")) conc_max_n = atoll(e);
@@ -886,7 +898,7 @@ std::shared_ptr<GraphEntry> build(OpK op, const Spec& spec, DView<const T> A, DV
   }
   const bool left = spec.side == RECTRI_CU_LEFT;
   const i64 rhs = left ? B.cols : B.rows;
-  const int P = g_prof.on ? 1 : panel_streams(rhs);
+  const int P = g_prof.on ? 1 : panel_streams(rhs, device_streams_pref<T>(rhs));
   if (P <= 1) {
     Recursion<T> rec(op, threshold, s, &g->events, &g->leaves);
     with_packs(rec).run(eff, A, B, 0);
